@@ -1,0 +1,350 @@
+"""Benchmark of the B200 PoisFFT solve path (driver contract: one JSON line on rank 0).
+
+Workload (N=1): BASELINE.json config c3 -- 512^3 fp64, staggered Neumann on all
+axes (DCT-II/III), FD2 eigenvalues, unit cube; the config the north-star's
+">= 60 % of HBM roofline" target is quoted on.  A "step" is one full solve of
+one 512^3 field resident in HBM (1 GiB in, 1 GiB out; larger than the 126 MB L2,
+so no explicit flush is needed between steps).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+--impl reference times the reference algorithm on the host cores (the oracle
+port in oracle/, which calls scipy.fft exactly like the reference) on the same
+workload.  Under torchrun every rank runs its own replica solve (no data-path
+collective): "replicas" scaling, see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Poisson solves/s & Gpoints/s (512³–2048³); % HBM/NVLink roofline at 1/2/4/8 GPU"
+WORKLOADS = {
+    "c3": "c3: 512^3 fp64 staggered-Neumann FD2 (DCT-II/III all axes), unit cube",
+    "c1": "c1: 64^3 fp64 periodic pseudo-spectral, L=2pi",
+    "c2": "c2: 4096^2 fp64 staggered-Dirichlet FD2 (DST-II/III)",
+    "c4": "c4: 1024x1024x512 fp64 periodic x,y + staggered-Neumann z, FD2",
+    "c5": "c5: 2048^3 fp32 periodic pseudo-spectral, L=2pi",
+}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_config(name):
+    import paper_1409_8116_b200 as fp
+    from oracle import fastpoisson_oracle as orc  # config table only (shapes / BCs)
+
+    case = orc.config_case(name)
+    grids = tuple(fp.GridSpec(a.n, a.length, fp.BoundaryCondition(a.bc), fp.GridKind(a.kind)) for a in case.axes)
+    return fp.SolverConfig(grids, fp.Approximation(case.approx), case.precision), case
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args, ws, rank):
+    """CPU reference arm: the reference algorithm (oracle port, scipy.fft) on all host cores."""
+    if rank != 0:
+        return
+    from oracle import fastpoisson_oracle as orc
+
+    case = orc.config_case(args.config)
+    rhs = orc.config_rhs(args.config, case, seed=0)
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        orc.solve(case, rhs, workers=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.solve(case, rhs, workers=cores)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    n_pts = int(np.prod(case.shape))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": case.dtype.name,
+        "data": "synthetic (seeded N(0,1), mean removed)",
+        "config": {"workload": WORKLOADS[args.config], "grid": list(case.shape)},
+        "gpoints_per_s": value * n_pts / 1e9,
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full {args.config} solves after {args.warmup} warm-up; "
+                                   "oracle/fastpoisson_oracle.solve (reference algorithm, scipy.fft workers=all cores)"},
+        "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(name, seconds_cap=30.0):
+    from oracle import fastpoisson_oracle as orc
+
+    case = orc.config_case(name)
+    rhs = orc.config_rhs(name, case, seed=0)
+    cores = len(os.sched_getaffinity(0))
+    orc.solve(case, rhs, workers=cores)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < 3 and (time.perf_counter() - t_start) < seconds_cap:
+        t0 = time.perf_counter()
+        orc.solve(case, rhs, workers=cores)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": 1.0 / med, "unit": "solves/s", "cores": cores, "kind": "port",
+            "sample": f"median of {len(times)} full {name} solves after 1 warm-up; oracle port of the reference "
+                      "algorithm (scipy.fft, workers=all cores) on this box's host"}
+
+
+def run_ours(args, ws, rank, local):
+    import ctypes
+
+    import torch
+
+    import paper_1409_8116_b200 as fp
+    from paper_1409_8116_b200 import _native as nat
+    from paper_1409_8116_b200 import _device as dv
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    config, case = make_config(args.config)
+    plan = fp.SolverPlan(config, device=dev)
+    lib = plan._lib
+    shape = config.shape
+    n_pts = int(np.prod(shape))
+    s = config.dtype.itemsize
+    tdt = dv.torch_dtype(config.dtype)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    rhs = torch.randn(shape, dtype=tdt, device=dev, generator=gen)
+    rhs -= rhs.mean()
+    out = torch.empty_like(rhs)
+    ws_bytes = plan.workspace_bytes(out_dense=True)
+    work = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    info = torch.zeros(16, dtype=torch.uint8, device=dev)
+    npass = plan.num_passes
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+
+    def make_events(k):
+        arr = (ctypes.c_void_p * k)()
+        for i in range(k):
+            h = ctypes.c_void_p()
+            nat.check(lib.fp_event_create(ctypes.byref(h)))
+            arr[i] = h
+        return arr
+
+    rs = nat.strides_array(rhs.stride())
+    os_ = nat.strides_array(out.stride())
+    rdt = dv.fp_dtype_of_torch(tdt)
+
+    def step(pass_ev=None):
+        nat.check(lib.fp_solve_ex(plan._handle, rhs.data_ptr(), rdt, rs, out.data_ptr(), os_, work.data_ptr(),
+                                  ws_bytes, sh, info.data_ptr(), None, pass_ev))
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize(dev)
+    pass_events = [make_events(npass + 1) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(pass_events[k])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if dist is not None:
+        tt = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+    # per-kernel durations (CUDA events on the launching stream)
+    per_pass = np.zeros((args.steps, npass))
+    ms = ctypes.c_float()
+    for k in range(args.steps):
+        for i in range(npass):
+            nat.check(lib.fp_event_elapsed_ms(pass_events[k][i], pass_events[k][i + 1], ctypes.byref(ms)))
+            per_pass[k, i] = ms.value
+    for arr in pass_events:
+        for i in range(npass + 1):
+            lib.fp_event_destroy(arr[i])
+    avg_pass = per_pass.mean(axis=0)
+    hbm_peak, peak_src = peaks()
+    pass_bytes = 2 * n_pts * s  # each pass reads and writes the field once
+    top = int(np.argmax(avg_pass))
+    ms_step = elapsed_ms / args.steps
+    value = ws * args.steps / (elapsed_ms * 1e-3)
+    b_alg = (2 * len(shape) - 1) * 2 * n_pts * s
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            tj = json.loads(prof.read_text())
+            traffic = tj.get(args.config, {}).get(str(top))
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "hbm",
+        "achieved": pass_bytes / (avg_pass[top] * 1e-3) / 1e9,
+        "peak": hbm_peak,
+        "unit": "GB/s",
+        "frac": pass_bytes / (avg_pass[top] * 1e-3) / 1e9 / hbm_peak,
+        "traffic": traffic,
+        "kernel": f"pass {top} of {npass}",
+        "algorithmic_bytes_per_launch": pass_bytes,
+        "peak_source": peak_src,
+        "per_pass_ms": [round(float(x), 4) for x in avg_pass],
+        "solve": {"algorithmic_bytes": b_alg, "achieved": b_alg / (ms_step * 1e-3) / 1e9,
+                  "frac": b_alg / (ms_step * 1e-3) / 1e9 / hbm_peak},
+    }
+    # e2e through the public API with pinned host buffers (H2D + solve + D2H each step)
+    rhs_host = torch.empty(shape, dtype=tdt, pin_memory=True)
+    rhs_host.copy_(rhs)
+    out_host = torch.empty(shape, dtype=tdt, pin_memory=True)
+    rhs_np, out_np = rhs_host.numpy(), out_host.numpy()
+    plan.solve(rhs_np, out=out_np)  # warm the path
+    e2e_steps = max(1, min(args.steps, 10))
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.solve(rhs_np, out=out_np)
+    e2e_dt = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_dt = float(tt.item())
+    e2e = {"value": ws * e2e_steps / e2e_dt, "unit": "solves/s", "h2d_bytes_per_step": n_pts * s,
+           "d2h_bytes_per_step": n_pts * s + 16, "path": "SolverPlan.solve(numpy pinned rhs, out=numpy pinned)"}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.config)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": config.dtype.name.replace("float", "f"),
+            "data": "synthetic (seeded N(0,1) field with its mean removed, generated on device)",
+            "config": {"workload": WORKLOADS[args.config], "grid": list(shape),
+                       "parallelism": "replicas" if ws > 1 else "single-gpu",
+                       "l2": "inputs (%.2f GiB/field) larger than L2; no flush" % (n_pts * s / 2**30)},
+            "gpoints_per_s": value * n_pts / 1e9,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": npass * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * fastpoisson_b200.h -- C ABI of the B200-native PoisFFT solve path.
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json
+ * (`SolverPlan.solve`, /root/reference/pkg/src/fastpoisson/solver.py:191-230).
+ * Every entry point takes plain pointers, sizes and integer enums; no torch or
+ * numpy type crosses it.  The Python host mirror (paper_1409_8116_b200/solver.py)
+ * binds it with ctypes; any other host can do the same.
+ *
+ * Reference interface replaced by each entry point (file:line in the reference):
+ *   fp_plan_create      SolverPlan.__init__            solver.py:136-181
+ *                       SolverConfig.__post_init__      solver.py:73-91
+ *                       GridSpec.__post_init__          grid.py:64-78
+ *   fp_plan_destroy     (Python GC of SolverPlan)
+ *   fp_plan_info        SolverConfig.mode/singular/periodic_axes  solver.py:105-119
+ *   fp_plan_workspace_bytes  per-call workspace of solve  solver.py:213 (work copy)
+ *   fp_solve            SolverPlan.solve (device buffers, async)  solver.py:191-230
+ *   fp_solve_ex         same, with per-kernel CUDA events (bench / profiling)
+ *   fp_solve_host       SolverPlan.solve (host buffers, sync)     solver.py:191-230
+ *   fp_removed_mean     SolveReport.removed_mean        solver.py:218-220
+ *   fp_transform_create TransformPlan(kind, n)          transforms.py:128-146
+ *   fp_transform_execute TransformPlan.execute_real/_complex transforms.py:157-172
+ *   fp_last_error       exception message of the failing call
+ *   fp_event_*          CUDA events behind SolveReport.timing (solver.py:215-228)
+ *
+ * Conventions
+ *   - Arrays are C order (last axis contiguous) unless strides say otherwise;
+ *     strides are in ELEMENTS of the array's own dtype and must be >= 0.
+ *   - fp_solve is asynchronous and stream-ordered on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream).  It never allocates: the caller passes a
+ *     workspace of at least fp_plan_workspace_bytes() bytes.
+ *   - Plans are immutable after creation; fp_solve on one plan from several
+ *     host threads is safe with distinct out/workspace/info buffers.
+ *   - `out` may be the same buffer as `rhs` (identical strides): in-place solve.
+ *   - Non-finite rhs values are detected on the device (flag in fp_solve_info);
+ *     fp_solve_host returns FP_ERR_NONFINITE before writing the host `out`.
+ */
+#ifndef FASTPOISSON_B200_H
+#define FASTPOISSON_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FP_API __attribute__((visibility("default")))
+#else
+#define FP_API
+#endif
+
+#define FP_ABI_VERSION 1
+
+typedef enum fp_status {
+    FP_OK = 0,
+    FP_ERR_CONFIG = 1,      /* ConfigurationError (grid.py:18-19)            */
+    FP_ERR_VALUE = 2,       /* ValueError: extents / strides / dtype         */
+    FP_ERR_UNSUPPORTED = 3, /* valid config this build cannot run            */
+    FP_ERR_CUDA = 4,        /* CUDA runtime failure                          */
+    FP_ERR_NONFINITE = 5,   /* ValueError("rhs contains non-finite values")  */
+    FP_ERR_ALLOC = 6        /* MemoryError                                   */
+} fp_status;
+
+/* BoundaryCondition (grid.py:22-25) */
+enum { FP_BC_PERIODIC = 0, FP_BC_DIRICHLET = 1, FP_BC_NEUMANN = 2 };
+/* GridKind (grid.py:28-30) */
+enum { FP_GRID_REGULAR = 0, FP_GRID_STAGGERED = 1 };
+/* Approximation (grid.py:33-37) */
+enum { FP_APPROX_SPECTRAL = 0, FP_APPROX_FD2 = 1 };
+/* element types */
+enum { FP_F64 = 0, FP_F32 = 1, FP_C128 = 2, FP_C64 = 3 };
+/* TransformKind (transforms.py:52-64) */
+enum {
+    FP_DFT = 0, FP_IDFT = 1,
+    FP_DST1 = 2, FP_DST2 = 3, FP_DST3 = 4,
+    FP_DCT1 = 5, FP_DCT2 = 6, FP_DCT3 = 7
+};
+
+/* SolverConfig: grids (GridSpec per axis) + approximation + precision. */
+typedef struct fp_config {
+    int ndim;               /* 1..3 */
+    int64_t n[3];           /* GridSpec.n      */
+    double length[3];       /* GridSpec.length */
+    int bc[3];              /* FP_BC_*         */
+    int kind[3];            /* FP_GRID_*       */
+    int approx;             /* FP_APPROX_*     */
+    int precision;          /* FP_F64 ("double") or FP_F32 ("single") */
+    /* Optional per-axis eigenvalue tables (n[a] doubles each), e.g. the host
+     * mirror's numpy tables; NULL = computed by the library (eigenvalues.py:51-83). */
+    const double* eig[3];
+} fp_config;
+
+typedef struct fp_plan fp_plan;
+typedef struct fp_transform fp_transform;
+
+typedef struct fp_plan_info {
+    int ndim;
+    int mode_mixed;         /* SolverConfig.mode == "mixed" */
+    int singular;           /* SolverConfig.singular        */
+    int periodic_mask;      /* bit a set <=> axis a periodic */
+    double null_scale;      /* _null_scale * prod(n_periodic) (solver.py:177-181,239) */
+    int num_passes;         /* kernel launches per solve     */
+    int middle_axis;        /* axis of the fused forward/scale/inverse pass */
+    int fft_axes_mask;      /* axes on the FFT engine (others: dense engine) */
+} fp_plan_info;
+
+/* Device-side per-solve record written by the kernels. */
+typedef struct fp_solve_info {
+    double dc;              /* raw null-mode coefficient (before scaling) */
+    int32_t nonfinite;      /* != 0 if rhs held NaN/Inf                   */
+    int32_t reserved;
+} fp_solve_info;
+
+typedef struct fp_solve_result {
+    double removed_mean;
+    double timing[3];       /* forward, diagonal, backward (seconds) */
+    double total_seconds;   /* including host<->device copies        */
+} fp_solve_result;
+
+FP_API int fp_abi_version(void);
+FP_API const char* fp_last_error(void);
+
+FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** plan);
+FP_API fp_status fp_plan_destroy(fp_plan* plan);
+FP_API fp_status fp_plan_info_get(const fp_plan* plan, fp_plan_info* info);
+/* out_dense != 0: the caller promises `out` is a dense C-order array that the
+ * solve may use as its real-valued scratch (smaller workspace). */
+FP_API fp_status fp_plan_workspace_bytes(const fp_plan* plan, int out_dense, size_t* bytes);
+
+/* Asynchronous device solve.  rhs_dtype: FP_F64 or FP_F32 (cast on load);
+ * out has the plan precision.  dev_info: device memory (zeroed by the call).
+ * phase_events: NULL or 4 cudaEvent_t recorded at start / after forward /
+ * after diagonal / end (SolveReport.timing keys, solver.py:215-228). */
+FP_API fp_status fp_solve(const fp_plan* plan,
+                          const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                          void* out, const int64_t* out_strides,
+                          void* workspace, size_t workspace_bytes,
+                          void* stream, fp_solve_info* dev_info,
+                          void* const* phase_events);
+
+/* fp_solve plus per-kernel events: pass_events (NULL or fp_plan_info.num_passes+1
+ * cudaEvent_t) are recorded before every kernel and after the last one. */
+FP_API fp_status fp_solve_ex(const fp_plan* plan,
+                             const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                             void* out, const int64_t* out_strides,
+                             void* workspace, size_t workspace_bytes,
+                             void* stream, fp_solve_info* dev_info,
+                             void* const* phase_events, void* const* pass_events);
+
+/* Synchronous host-buffer solve (H2D, fp_solve, D2H); returns FP_ERR_NONFINITE
+ * without touching `out` when rhs holds NaN/Inf. */
+FP_API fp_status fp_solve_host(const fp_plan* plan,
+                               const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                               void* out, const int64_t* out_strides,
+                               fp_solve_result* result);
+
+/* removed_mean from a host copy of the device record (solver.py:218-220). */
+FP_API fp_status fp_removed_mean(const fp_plan* plan, const fp_solve_info* host_info,
+                                 double* removed_mean);
+
+/* 1D transform of one kind and length along `axis` of an up-to-3D array. */
+FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int device,
+                                     fp_transform** t);
+FP_API fp_status fp_transform_destroy(fp_transform* t);
+FP_API fp_status fp_transform_execute(const fp_transform* t, int ndim, const int64_t* shape,
+                                      int axis,
+                                      const void* in, int in_dtype, const int64_t* in_strides,
+                                      void* out, int out_dtype, const int64_t* out_strides,
+                                      void* stream);
+
+/* CUDA event helpers for SolveReport.timing (phase_events of fp_solve). */
+FP_API fp_status fp_event_create(void** event);
+FP_API fp_status fp_event_destroy(void* event);
+FP_API fp_status fp_event_elapsed_ms(void* start, void* stop, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTPOISSON_B200_H */

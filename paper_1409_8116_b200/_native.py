@@ -1,0 +1,154 @@
+"""ctypes binding of the C ABI in ``include/fastpoisson_b200.h``.
+
+This is the only place the Python host mirror touches native code.  The
+library is loaded lazily; a missing or unloadable library raises immediately
+(there is no CPU fallback for the solve path).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from ctypes import POINTER, Structure, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p, c_char_p
+
+from ._build import LIB_PATH
+
+FP_OK = 0
+FP_ERR_CONFIG = 1
+FP_ERR_VALUE = 2
+FP_ERR_UNSUPPORTED = 3
+FP_ERR_CUDA = 4
+FP_ERR_NONFINITE = 5
+FP_ERR_ALLOC = 6
+
+FP_BC_PERIODIC, FP_BC_DIRICHLET, FP_BC_NEUMANN = 0, 1, 2
+FP_GRID_REGULAR, FP_GRID_STAGGERED = 0, 1
+FP_APPROX_SPECTRAL, FP_APPROX_FD2 = 0, 1
+FP_F64, FP_F32, FP_C128, FP_C64 = 0, 1, 2, 3
+FP_DFT, FP_IDFT, FP_DST1, FP_DST2, FP_DST3, FP_DCT1, FP_DCT2, FP_DCT3 = range(8)
+
+
+class FpConfig(Structure):
+    _fields_ = [
+        ("ndim", c_int),
+        ("n", c_int64 * 3),
+        ("length", c_double * 3),
+        ("bc", c_int * 3),
+        ("kind", c_int * 3),
+        ("approx", c_int),
+        ("precision", c_int),
+        ("eig", POINTER(c_double) * 3),
+    ]
+
+
+class FpPlanInfo(Structure):
+    _fields_ = [
+        ("ndim", c_int),
+        ("mode_mixed", c_int),
+        ("singular", c_int),
+        ("periodic_mask", c_int),
+        ("null_scale", c_double),
+        ("num_passes", c_int),
+        ("middle_axis", c_int),
+        ("fft_axes_mask", c_int),
+    ]
+
+
+class FpSolveInfo(Structure):
+    _fields_ = [("dc", c_double), ("nonfinite", c_int32), ("reserved", c_int32)]
+
+
+class FpSolveResult(Structure):
+    _fields_ = [("removed_mean", c_double), ("timing", c_double * 3), ("total_seconds", c_double)]
+
+
+# symbol -> (restype, argtypes); the CPU test tier checks every one is exported
+SIGNATURES = {
+    "fp_abi_version": (c_int, []),
+    "fp_last_error": (c_char_p, []),
+    "fp_plan_create": (c_int, [POINTER(FpConfig), c_int, POINTER(c_void_p)]),
+    "fp_plan_destroy": (c_int, [c_void_p]),
+    "fp_plan_info_get": (c_int, [c_void_p, POINTER(FpPlanInfo)]),
+    "fp_plan_workspace_bytes": (c_int, [c_void_p, c_int, POINTER(c_size_t)]),
+    "fp_solve": (
+        c_int,
+        [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_size_t,
+         c_void_p, c_void_p, POINTER(c_void_p)],
+    ),
+    "fp_solve_ex": (
+        c_int,
+        [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_size_t,
+         c_void_p, c_void_p, POINTER(c_void_p), POINTER(c_void_p)],
+    ),
+    "fp_solve_host": (
+        c_int,
+        [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), POINTER(FpSolveResult)],
+    ),
+    "fp_removed_mean": (c_int, [c_void_p, POINTER(FpSolveInfo), POINTER(c_double)]),
+    "fp_transform_create": (c_int, [c_int, c_int64, c_int, c_int, POINTER(c_void_p)]),
+    "fp_transform_destroy": (c_int, [c_void_p]),
+    "fp_transform_execute": (
+        c_int,
+        [c_void_p, c_int, POINTER(c_int64), c_int, c_void_p, c_int, POINTER(c_int64), c_void_p, c_int,
+         POINTER(c_int64), c_void_p],
+    ),
+    "fp_event_create": (c_int, [POINTER(c_void_p)]),
+    "fp_event_destroy": (c_int, [c_void_p]),
+    "fp_event_elapsed_ms": (c_int, [c_void_p, c_void_p, POINTER(c_float)]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path=None):
+    """Load (once) and return the native library; raises if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = str(path or LIB_PATH)
+        try:
+            lib = ctypes.CDLL(p)
+        except OSError as exc:
+            raise RuntimeError(
+                f"native library {p} is not loadable ({exc}); build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` -- the solve path has no CPU fallback"
+            ) from None
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().fp_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = ""):
+    """Map an fp_status to the reference's exception types."""
+    if status == FP_OK:
+        return
+    from .grid import ConfigurationError
+
+    msg = last_error() or what
+    if status == FP_ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if status in (FP_ERR_VALUE, FP_ERR_NONFINITE):
+        raise ValueError(msg)
+    if status == FP_ERR_ALLOC:
+        raise MemoryError(msg)
+    if status == FP_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+def strides_array(strides):
+    arr = (c_int64 * 3)()
+    for i, s in enumerate(strides):
+        arr[i] = int(s)
+    return arr

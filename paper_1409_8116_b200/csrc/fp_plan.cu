@@ -1,0 +1,993 @@
+// fp_plan.cu -- plan construction, pass scheduling and the C ABI
+// (include/fastpoisson_b200.h).
+//
+// Reference behaviour mirrored here:
+//   SolverConfig validation          solver.py:73-91, grid.py:64-78
+//   pair table / backward scales     transforms.py:88-125
+//   eigenvalue tables                eigenvalues.py:51-83
+//   null-mode bookkeeping            solver.py:56-62,177-181,218-220
+//   solve pipeline                   solver.py:191-249
+// The pipeline is re-planned for HBM: real axes first (contiguous axis first),
+// then the periodic axes (the first one as a real FFT -> half spectrum), and
+// the LAST forward axis runs as one fused MID pass (forward, scale, inverse).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fastpoisson_b200.h"
+#include "fp_tables.h"
+#include "fp_types.h"
+
+namespace fpb {
+cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st);
+cudaError_t launch_dense_pass(const DensePass& p, bool f32, cudaStream_t st);
+cudaError_t launch_scale_pass(const ScalePass& p, bool f32, cudaStream_t st);
+cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st);
+size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
+}  // namespace fpb
+
+using namespace fpb;
+
+static thread_local std::string g_err;
+static fp_status fail(fp_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(FP_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+namespace {
+
+enum Buf { B_RHS = 0, B_OUT = 1, B_RS = 2, B_CW = 3 };
+enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2 };
+enum Layout { LY_REAL = 0, LY_CPLX = 1 };  // state of the data in the buffer
+
+struct DevTables {
+    void* wfft = nullptr;
+    void* wt = nullptr;
+    void* ww = nullptr;
+    void* mat_f = nullptr;  // dense forward
+    void* mat_b = nullptr;  // dense backward
+    int fwd_nout = 0, fwd_nin = 0, bwd_nout = 0, bwd_nin = 0;
+    bool fwd_cpx = false, bwd_cpx = false;
+};
+
+struct PassT {
+    int engine;
+    int phase;           // 0 forward, 1 diagonal, 2 backward
+    int t;               // transform axis (-1 for scale)
+    int in_buf, out_buf;
+    int in_layout, out_layout;
+    FftPass fp;
+    DensePass dp;
+    ScalePass sp;
+    int a, b;            // other axes (-1 = dummy)
+};
+
+// strides per axis for a buffer state (elements)
+struct Strides {
+    long long s[3];
+};
+
+}  // namespace
+
+struct fp_plan {
+    int device = 0;
+    fp_config cfg{};
+    int ndim = 0;
+    bool f32 = false;
+    bool singular = false;
+    bool mixed = false;
+    int periodic_mask = 0;
+    int r_axis = -1;          // periodic axis transformed as real FFT (half spectrum)
+    int middle = -1;
+    int fft_mask = 0;
+    long long n[3] = {1, 1, 1};
+    long long cext[3] = {1, 1, 1};   // complex-state extents (r axis = n/2+1)
+    long long cpitch_last = 1;       // padded contiguous extent of the complex buffer
+    bool need_cw = false, need_rs = false;
+    bool mean_fix = false;           // exact arithmetic-mean removal (DCT-I axes)
+    double bscale = 1.0;
+    double np_prod = 1.0;
+    double null_scale = 1.0;
+    std::vector<PassT> passes;
+    DevTables tab[3];
+    double* d_lam[3] = {nullptr, nullptr, nullptr};
+    std::vector<void*> allocs;
+    ~fp_plan() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+        cudaSetDevice(prev);
+    }
+};
+
+struct fp_transform {
+    int device = 0;
+    int kind = 0;
+    long long n = 0;
+    bool f32 = false;
+    bool fft = false;
+    int M = 0;
+    DevTables tab;
+    std::vector<void*> allocs;
+    ~fp_transform() {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        for (void* p : allocs) cudaFree(p);
+        cudaSetDevice(prev);
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+int ilog2(long long x) { int l = 0; while ((1LL << l) < x) ++l; return l; }
+
+// upload a long double table rounded to the plan precision (complex pairs or reals)
+template <typename AllocT>
+fp_status upload(AllocT& allocs, const std::vector<long double>& v, bool f32, void** out) {
+    *out = nullptr;
+    if (v.empty()) return FP_OK;
+    const size_t cnt = v.size();
+    void* d = nullptr;
+    if (f32) {
+        std::vector<float> h(cnt);
+        for (size_t i = 0; i < cnt; ++i) h[i] = (float)v[i];
+        CUDA_TRY(cudaMalloc(&d, cnt * sizeof(float)));
+        allocs.push_back(d);
+        CUDA_TRY(cudaMemcpy(d, h.data(), cnt * sizeof(float), cudaMemcpyHostToDevice));
+    } else {
+        std::vector<double> h(cnt);
+        for (size_t i = 0; i < cnt; ++i) h[i] = (double)v[i];
+        CUDA_TRY(cudaMalloc(&d, cnt * sizeof(double)));
+        allocs.push_back(d);
+        CUDA_TRY(cudaMemcpy(d, h.data(), cnt * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    *out = d;
+    return FP_OK;
+}
+
+// forward/backward transform ids of a (bc, kind) row (transforms.py:99-125)
+void pair_for(int bc, int kind, int* fwd, int* bwd) {
+    if (bc == FP_BC_PERIODIC) { *fwd = FP_DFT; *bwd = FP_IDFT; }
+    else if (bc == FP_BC_DIRICHLET) {
+        if (kind == FP_GRID_REGULAR) { *fwd = FP_DST1; *bwd = FP_DST1; }
+        else { *fwd = FP_DST2; *bwd = FP_DST3; }
+    } else {
+        if (kind == FP_GRID_REGULAR) { *fwd = FP_DCT1; *bwd = FP_DCT1; }
+        else { *fwd = FP_DCT2; *bwd = FP_DCT3; }
+    }
+}
+
+double backward_scale(int fwd, long long n) {  // transforms.py:88-96
+    if (fwd == FP_DFT) return 1.0;
+    if (fwd == FP_DST1) return 1.0 / (2.0 * (double)(n + 1));
+    if (fwd == FP_DCT1) return 1.0 / (2.0 * (double)(n - 1));
+    return 1.0 / (2.0 * (double)n);
+}
+
+double ones_null_coeff(int fwd, long long n) {  // solver.py:58-62
+    if (fwd == FP_DFT) return 1.0;
+    if (fwd == FP_DCT1) return 2.0 * (double)(n - 1);
+    return 2.0 * (double)n;
+}
+
+fp_status validate(const fp_config* c) {
+    if (!c) return fail(FP_ERR_CONFIG, "config is NULL");
+    if (c->ndim < 1 || c->ndim > 3)
+        return fail(FP_ERR_CONFIG, "1 to 3 dimensions supported, got " + std::to_string(c->ndim));
+    if (c->precision != FP_F64 && c->precision != FP_F32)
+        return fail(FP_ERR_CONFIG, "precision must be one of ['double', 'single']");
+    if (c->approx != FP_APPROX_SPECTRAL && c->approx != FP_APPROX_FD2)
+        return fail(FP_ERR_CONFIG, "unknown approximation");
+    int nrow_bc = -1, nrow_kind = -1;
+    for (int a = 0; a < c->ndim; ++a) {
+        const long long n = c->n[a];
+        if (n < 1) return fail(FP_ERR_CONFIG, "point count must be positive, got n=" + std::to_string(n));
+        if (!(c->length[a] > 0.0)) return fail(FP_ERR_CONFIG, "axis length must be positive");
+        if (c->bc[a] < 0 || c->bc[a] > 2 || c->kind[a] < 0 || c->kind[a] > 1)
+            return fail(FP_ERR_CONFIG, "unknown boundary condition or grid kind");
+        if (c->bc[a] == FP_BC_PERIODIC && c->kind[a] == FP_GRID_STAGGERED)
+            return fail(FP_ERR_CONFIG, "periodic boundary conditions admit only the regular grid");
+        if (c->bc[a] == FP_BC_NEUMANN && c->kind[a] == FP_GRID_REGULAR && n < 2)
+            return fail(FP_ERR_CONFIG, "Neumann on a regular grid needs n >= 2 (boundary nodes included)");
+        if (c->bc[a] != FP_BC_PERIODIC) {
+            if (nrow_bc < 0) { nrow_bc = c->bc[a]; nrow_kind = c->kind[a]; }
+            else if (nrow_bc != c->bc[a] || nrow_kind != c->kind[a])
+                return fail(FP_ERR_CONFIG,
+                            "unsupported boundary pattern: non-periodic axes must all carry the same "
+                            "condition and grid kind");
+        }
+        if (n > (1LL << 30)) return fail(FP_ERR_UNSUPPORTED, "axis too long");
+    }
+    return FP_OK;
+}
+
+// Which engine runs the transform along an axis, and its FFT length.
+// rfft: axis is the real-FFT periodic axis.  Returns M (0 = dense).
+int fft_length(int bc, int kind, long long n, bool rfft) {
+    if (bc == FP_BC_PERIODIC) {
+        const long long M = rfft ? ((n % 2 == 0) ? n / 2 : 0) : n;
+        if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+        return 0;
+    }
+    if (kind != FP_GRID_STAGGERED) return 0;  // DST-I / DCT-I: dense engine
+    if (n % 2) return 0;
+    const long long M = n / 2;
+    if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+    return 0;
+}
+
+const long long kDenseMax = 4096;
+
+// choose the tile shape of an FFT pass
+void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long nb) {
+    const int logTL = p.logM - 4;
+    const int real_bytes = f32 ? 4 : 8;
+    int lines;
+    if (p.family == FAM_CONTIG) {
+        lines = std::max(1, 256 >> logTL);
+        const long long nl = na * nb;
+        while (lines > 1 && lines / 2 >= nl) lines /= 2;
+        p.lines = lines;
+        p.logLines = ilog2(lines);
+        while (p.lines > 1 && fft_pass_smem_bytes(p, real_bytes) > 100 * 1024) {
+            p.lines /= 2;
+            p.logLines -= 1;
+        }
+        p.tiles = (int)((nl + p.lines - 1) / p.lines);
+        p.nbt = 0;
+    } else {
+        const int eb = (in_cpx ? 2 : 1) * real_bytes;
+        lines = std::max(1, 128 / eb);
+        while (lines > 1 && lines / 2 >= nb) lines /= 2;
+        p.lines = lines;
+        p.logLines = ilog2(lines);
+        while (p.lines > 1 && ((p.lines << logTL) > (f32 ? 1024 : 512) || fft_pass_smem_bytes(p, real_bytes) > 200 * 1024)) {
+            p.lines /= 2;
+            p.logLines -= 1;
+        }
+        p.nbt = (int)((nb + p.lines - 1) / p.lines);
+        p.tiles = (int)(na * p.nbt);
+    }
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+FP_API int fp_abi_version(void) { return FP_ABI_VERSION; }
+FP_API const char* fp_last_error(void) { return g_err.c_str(); }
+
+FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out) {
+    if (!out) return fail(FP_ERR_VALUE, "plan out-pointer is NULL");
+    *out = nullptr;
+    fp_status st = validate(cfg);
+    if (st != FP_OK) return st;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(FP_ERR_CUDA, "no CUDA device available (the solve path has no CPU fallback)");
+    if (device < 0 || device >= ndev) return fail(FP_ERR_VALUE, "invalid device ordinal");
+    DeviceGuard dg(device);
+
+    fp_plan* P = new fp_plan();
+    P->device = device;
+    P->cfg = *cfg;
+    const int d = cfg->ndim;
+    P->ndim = d;
+    P->f32 = cfg->precision == FP_F32;
+    int fwd[3] = {0, 0, 0}, bwd[3] = {0, 0, 0};
+    P->singular = true;
+    for (int a = 0; a < d; ++a) {
+        P->n[a] = cfg->n[a];
+        pair_for(cfg->bc[a], cfg->kind[a], &fwd[a], &bwd[a]);
+        if (cfg->bc[a] == FP_BC_PERIODIC) P->periodic_mask |= 1 << a;
+        if (cfg->bc[a] == FP_BC_DIRICHLET) P->singular = false;
+        P->bscale *= backward_scale(fwd[a], cfg->n[a]);
+        if (cfg->bc[a] == FP_BC_PERIODIC) P->np_prod *= (double)cfg->n[a];
+    }
+    {   // SolverConfig.mode (solver.py:111-114): uniform iff one (bc, kind) row
+        bool uniform = true;
+        for (int a = 1; a < d; ++a) if (cfg->bc[a] != cfg->bc[0] || cfg->kind[a] != cfg->kind[0]) uniform = false;
+        P->mixed = !uniform;
+    }
+    if (P->singular) {
+        // solver.py:224-225: the reference subtracts the arithmetic mean after the
+        // backward pass.  With DFT / DCT-II the zeroed null coefficient already IS
+        // the mean (no-op to roundoff); with DCT-I it is a trapezoid-weighted mean,
+        // so those plans get the explicit reduction + subtraction.
+        for (int a = 0; a < d; ++a)
+            if (cfg->bc[a] == FP_BC_NEUMANN && cfg->kind[a] == FP_GRID_REGULAR) P->mean_fix = true;
+        double ns = 1.0;
+        for (int a = 0; a < d; ++a) ns *= ones_null_coeff(fwd[a], cfg->n[a]);
+        P->null_scale = ns;
+    }
+
+    // forward order: real axes descending, then periodic axes descending
+    std::vector<int> order;
+    for (int a = d - 1; a >= 0; --a) if (cfg->bc[a] != FP_BC_PERIODIC) order.push_back(a);
+    for (int a = d - 1; a >= 0; --a) if (cfg->bc[a] == FP_BC_PERIODIC) { if (P->r_axis < 0) P->r_axis = a; order.push_back(a); }
+    P->middle = order.back();
+    for (int a = 0; a < 3; ++a) P->cext[a] = P->n[a];
+    if (P->r_axis >= 0) P->cext[P->r_axis] = P->n[P->r_axis] / 2 + 1;
+    P->cpitch_last = (P->cext[d - 1] + 7) / 8 * 8;
+    if (P->r_axis < 0 || P->cext[d - 1] == P->n[d - 1]) P->cpitch_last = P->cext[d - 1];
+
+    // eigenvalue tables (host mirror may pass numpy-built ones)
+    for (int a = 0; a < d; ++a) {
+        std::vector<double> lam;
+        if (cfg->eig[a]) lam.assign(cfg->eig[a], cfg->eig[a] + cfg->n[a]);
+        else lam = eigenvalue_table(AxisSpec{cfg->n[a], cfg->length[a], cfg->bc[a], cfg->kind[a]}, cfg->approx);
+        void* dl = nullptr;
+        if (cudaMalloc(&dl, lam.size() * sizeof(double)) != cudaSuccess) { delete P; return fail(FP_ERR_ALLOC, "cudaMalloc eigenvalue table"); }
+        P->allocs.push_back(dl);
+        if (cudaMemcpy(dl, lam.data(), lam.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) { delete P; return fail(FP_ERR_CUDA, "upload eigenvalue table"); }
+        P->d_lam[a] = (double*)dl;
+    }
+
+    // per-axis engines + tables
+    int Mx[3] = {0, 0, 0};
+    for (int a = 0; a < d; ++a) {
+        const bool rf = (a == P->r_axis);
+        Mx[a] = fft_length(cfg->bc[a], cfg->kind[a], cfg->n[a], rf);
+        DevTables& T = P->tab[a];
+        if (Mx[a] > 0) {
+            P->fft_mask |= 1 << a;
+            std::vector<long double> wf, wt, ww;
+            const bool real_kind = cfg->bc[a] != FP_BC_PERIODIC || rf;
+            fft_tables((int)cfg->n[a], Mx[a], real_kind, wf, wt, ww);
+            if ((st = upload(P->allocs, wf, P->f32, &T.wfft)) != FP_OK) { delete P; return st; }
+            if ((st = upload(P->allocs, wt, P->f32, &T.wt)) != FP_OK) { delete P; return st; }
+            if ((st = upload(P->allocs, ww, P->f32, &T.ww)) != FP_OK) { delete P; return st; }
+        } else {
+            if (cfg->n[a] > kDenseMax) {
+                delete P;
+                return fail(FP_ERR_UNSUPPORTED, "axis length " + std::to_string(cfg->n[a]) +
+                                                    " needs the dense engine, limited to n <= 4096 in this build");
+            }
+            std::vector<long double> m;
+            int no, ni;
+            bool cpx;
+            const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
+            const int bk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 101 : FP_IDFT) : bwd[a];
+            dense_matrix(fk, (int)cfg->n[a], m, &no, &ni, &cpx);
+            T.fwd_nout = no; T.fwd_nin = ni; T.fwd_cpx = cpx;
+            if ((st = upload(P->allocs, m, P->f32, &T.mat_f)) != FP_OK) { delete P; return st; }
+            dense_matrix(bk, (int)cfg->n[a], m, &no, &ni, &cpx);
+            T.bwd_nout = no; T.bwd_nin = ni; T.bwd_cpx = cpx;
+            if ((st = upload(P->allocs, m, P->f32, &T.mat_b)) != FP_OK) { delete P; return st; }
+        }
+    }
+
+    // ---- pass schedule
+    // extents of the state: before the r-axis forward pass (and after its
+    // inverse) everything is real with extents n; in between, complex with cext.
+    auto other_axes = [&](int t, int* a_, int* b_) {
+        int o[2] = {-1, -1}, k = 0;
+        for (int a = 0; a < d; ++a) if (a != t) o[k++] = a;
+        if (k == 2) { *a_ = o[0]; *b_ = o[1]; }
+        else if (k == 1) { *a_ = -1; *b_ = o[0]; }
+        else { *a_ = -1; *b_ = -1; }
+    };
+    const double inv_np = 1.0 / P->np_prod;
+    bool complex_state = false;
+    int cur = B_RHS;
+    const int realbuf = B_RS;  // resolved at solve time to OUT when out is dense
+
+    auto make_fft = [&](int t, int op, bool in_cpx, bool out_cpx, int in_buf, int out_buf, int phase) {
+        PassT ps{};
+        ps.engine = EN_FFT;
+        ps.phase = phase;
+        ps.t = t;
+        ps.in_buf = in_buf;
+        ps.out_buf = out_buf;
+        ps.in_layout = in_cpx ? LY_CPLX : LY_REAL;
+        ps.out_layout = out_cpx ? LY_CPLX : LY_REAL;
+        other_axes(t, &ps.a, &ps.b);
+        FftPass& p = ps.fp;
+        const bool periodic = cfg->bc[t] == FP_BC_PERIODIC;
+        const bool rf = t == P->r_axis;
+        p.op = op;
+        p.fkind = periodic ? (rf ? FK_RFFT : FK_CFFT) : (cfg->bc[t] == FP_BC_DIRICHLET ? FK_DST2 : FK_DCT2);
+        p.ikind = periodic ? (rf ? IK_IRFFT : IK_ICFFT) : (cfg->bc[t] == FP_BC_DIRICHLET ? IK_DST3 : IK_DCT3);
+        p.family = (t == d - 1) ? FAM_CONTIG : FAM_STRIDED;
+        p.n = (int)cfg->n[t];
+        p.M = Mx[t];
+        p.logM = ilog2(p.M);
+        p.ls = p.M + p.M / 16 + 1;
+        if ((p.ls & 1) == 0) p.ls += 1;
+        const long long* ext = complex_state ? P->cext : P->n;
+        const long long na = ps.a >= 0 ? ext[ps.a] : 1;
+        const long long nb = ps.b >= 0 ? ext[ps.b] : 1;
+        p.g.na = (int)na;
+        p.g.nb = (int)nb;
+        fft_tile_shape(p, P->f32, in_cpx, na, nb);
+        p.wfft = P->tab[t].wfft;
+        p.wt = P->tab[t].wt;
+        p.ww = P->tab[t].ww;
+        p.out_mult = 1.0;
+        Scaling& s = p.s;
+        s.lam_t = P->d_lam[t];
+        s.lam_a = ps.a >= 0 ? P->d_lam[ps.a] : nullptr;
+        s.lam_b = ps.b >= 0 ? P->d_lam[ps.b] : nullptr;
+        s.pos_t = t; s.pos_a = ps.a; s.pos_b = ps.b;
+        s.bscale = P->bscale;
+        s.inv_np = inv_np;
+        s.singular = P->singular;
+        return ps;
+    };
+    auto make_dense = [&](int t, bool forward, bool in_cpx, bool out_cpx, int in_buf, int out_buf, int phase) {
+        PassT ps{};
+        ps.engine = EN_DENSE;
+        ps.phase = phase;
+        ps.t = t;
+        ps.in_buf = in_buf;
+        ps.out_buf = out_buf;
+        ps.in_layout = in_cpx ? LY_CPLX : LY_REAL;
+        ps.out_layout = out_cpx ? LY_CPLX : LY_REAL;
+        other_axes(t, &ps.a, &ps.b);
+        DensePass& p = ps.dp;
+        const DevTables& T = P->tab[t];
+        p.n_in = forward ? T.fwd_nin : T.bwd_nin;
+        p.n_out = forward ? T.fwd_nout : T.bwd_nout;
+        p.mat = forward ? T.mat_f : T.mat_b;
+        p.cls = !in_cpx && !out_cpx ? DC_R2R : (!in_cpx ? DC_R2C : (out_cpx ? DC_C2C : DC_C2R));
+        const long long* ext = complex_state ? P->cext : P->n;
+        const long long na = ps.a >= 0 ? ext[ps.a] : 1;
+        const long long nb = ps.b >= 0 ? ext[ps.b] : 1;
+        p.g.na = (int)na;
+        p.g.nb = (int)nb;
+        p.in_ls = in_cpx ? 2 * p.n_in : p.n_in;
+        const int rb = P->f32 ? 4 : 8;
+        int lines = std::max(1, (48 * 1024) / (p.in_ls * rb));
+        lines = std::min(lines, 64);
+        const long long nl = na * nb;
+        if (lines > nl) lines = (int)nl;
+        p.lines = lines;
+        p.tiles = (int)((nl + lines - 1) / lines);
+        p.out_mult = 1.0;
+        return ps;
+    };
+    auto make_scale = [&](int phase, int buf, bool cpx) {
+        PassT ps{};
+        ps.engine = EN_SCALE;
+        ps.phase = phase;
+        ps.t = -1;
+        ps.in_buf = ps.out_buf = buf;
+        ps.in_layout = ps.out_layout = cpx ? LY_CPLX : LY_REAL;
+        ps.a = ps.b = -1;
+        ScalePass& s = ps.sp;
+        s.ndim = d;
+        for (int a = 0; a < 3; ++a) s.lam[a] = a < d ? P->d_lam[a] : nullptr;
+        s.bscale = P->bscale;
+        s.inv_np = inv_np;
+        s.singular = P->singular;
+        return ps;
+    };
+
+    const bool only_middle = order.size() == 1;
+    // forward passes
+    for (size_t i = 0; i + 1 < order.size(); ++i) {
+        const int t = order[i];
+        const bool rf = t == P->r_axis;
+        const bool in_cpx = complex_state;
+        const bool out_cpx = complex_state || rf;
+        const int dst = out_cpx ? B_CW : realbuf;
+        if (out_cpx) P->need_cw = true; else P->need_rs = true;
+        if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_FWD, in_cpx, out_cpx, cur, dst, 0));
+        else P->passes.push_back(make_dense(t, true, in_cpx, out_cpx, cur, dst, 0));
+        if (rf) complex_state = true;
+        cur = dst;
+    }
+    // middle
+    {
+        const int t = P->middle;
+        const bool rf = t == P->r_axis;
+        const int dst = only_middle ? B_OUT : cur;
+        if (Mx[t] > 0) {
+            P->passes.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
+        } else if (!rf) {
+            // dense forward, scale, dense inverse on the same buffer
+            int work = cur;
+            if (only_middle) work = complex_state ? B_CW : realbuf;
+            if (only_middle && !complex_state) P->need_rs = true;
+            P->passes.push_back(make_dense(t, true, complex_state, complex_state, cur, work, 1));
+            P->passes.push_back(make_scale(1, work, complex_state));
+            P->passes.push_back(make_dense(t, false, complex_state, complex_state, work, dst, 1));
+        } else {
+            // real-FFT middle axis on the dense engine: real -> half spectrum -> real
+            P->need_cw = true;
+            P->passes.push_back(make_dense(t, true, false, true, cur, B_CW, 1));
+            complex_state = true;
+            P->passes.push_back(make_scale(1, B_CW, true));
+            // the inverse writes real data: extents of other axes unchanged
+            PassT inv = make_dense(t, false, true, false, B_CW, dst, 1);
+            P->passes.push_back(inv);
+            complex_state = false;
+        }
+    }
+    // backward passes
+    for (int i = (int)order.size() - 2; i >= 0; --i) {
+        const int t = order[i];
+        const bool rf = t == P->r_axis;
+        const bool in_cpx = complex_state;
+        const bool out_cpx = complex_state && !rf;
+        const bool last = i == 0;
+        const int dst = last ? B_OUT : (out_cpx ? B_CW : (in_cpx ? realbuf : cur));
+        if (!out_cpx && !last) P->need_rs = true;
+        if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_INV, in_cpx, out_cpx, cur, dst, 2));
+        else P->passes.push_back(make_dense(t, false, in_cpx, out_cpx, cur, dst, 2));
+        if (rf) complex_state = false;
+        cur = dst;
+    }
+    // the first pass checks finiteness of the rhs (solver.py:201-202)
+    *out = P;
+    return FP_OK;
+}
+
+FP_API fp_status fp_plan_destroy(fp_plan* plan) {
+    delete plan;
+    return FP_OK;
+}
+
+FP_API fp_status fp_plan_info_get(const fp_plan* P, fp_plan_info* info) {
+    if (!P || !info) return fail(FP_ERR_VALUE, "NULL argument");
+    info->ndim = P->ndim;
+    info->mode_mixed = P->mixed;
+    info->singular = P->singular;
+    info->periodic_mask = P->periodic_mask;
+    info->null_scale = P->null_scale * P->np_prod;
+    info->num_passes = (int)P->passes.size();  // + 3 small launches when mean_fix
+    info->middle_axis = P->middle;
+    info->fft_axes_mask = P->fft_mask;
+    return FP_OK;
+}
+
+static size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
+
+static size_t cw_bytes(const fp_plan* P) {
+    if (!P->need_cw) return 0;
+    size_t cnt = 1;
+    for (int a = 0; a < P->ndim - 1; ++a) cnt *= (size_t)P->cext[a];
+    cnt *= (size_t)P->cpitch_last;
+    return align_up(cnt * 2 * (P->f32 ? 4 : 8));
+}
+static size_t rs_bytes(const fp_plan* P) {
+    size_t cnt = 1;
+    for (int a = 0; a < P->ndim; ++a) cnt *= (size_t)P->n[a];
+    return align_up(cnt * (P->f32 ? 4 : 8));
+}
+
+static size_t mean_bytes(const fp_plan* P) {
+    return P->mean_fix ? align_up((size_t)(kMeanParts + 1) * sizeof(double)) : 0;
+}
+
+FP_API fp_status fp_plan_workspace_bytes(const fp_plan* P, int out_dense, size_t* bytes) {
+    if (!P || !bytes) return fail(FP_ERR_VALUE, "NULL argument");
+    size_t b = cw_bytes(P);
+    if (P->need_rs && !out_dense) b += rs_bytes(P);
+    b += mean_bytes(P);
+    *bytes = b;
+    return FP_OK;
+}
+
+static void dense_strides(const fp_plan* P, bool cpx, long long s[3]) {
+    const int d = P->ndim;
+    long long acc = 1;
+    for (int a = d - 1; a >= 0; --a) {
+        s[a] = acc;
+        if (cpx) acc *= (a == d - 1) ? P->cpitch_last : P->cext[a];
+        else acc *= P->n[a];
+    }
+    for (int a = d; a < 3; ++a) s[a] = 0;
+}
+
+FP_API fp_status fp_solve(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                          void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
+                          void* stream, fp_solve_info* dev_info, void* const* phase_events) {
+    return fp_solve_ex(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
+                       dev_info, phase_events, nullptr);
+}
+
+FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
+                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
+                             void* const* pass_events) {
+    if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
+    if (!rhs || !out) return fail(FP_ERR_VALUE, "rhs/out is NULL");
+    if (rhs_dtype != FP_F64 && rhs_dtype != FP_F32) return fail(FP_ERR_VALUE, "rhs dtype must be f64 or f32");
+    const int d = P->ndim;
+    long long dense_r[3];
+    dense_strides(P, false, dense_r);
+    long long rs_s[3], os_s[3], cw_s[3];
+    for (int a = 0; a < 3; ++a) {
+        rs_s[a] = (a < d) ? (rhs_strides ? rhs_strides[a] : dense_r[a]) : 0;
+        os_s[a] = (a < d) ? (out_strides ? out_strides[a] : dense_r[a]) : 0;
+        if (a < d && (rs_s[a] < 0 || os_s[a] < 0)) return fail(FP_ERR_VALUE, "negative strides are not supported");
+    }
+    dense_strides(P, true, cw_s);
+    bool out_dense = true;
+    for (int a = 0; a < d; ++a) if (P->n[a] > 1 && os_s[a] != dense_r[a]) out_dense = false;
+    size_t need = 0;
+    fp_plan_workspace_bytes(P, out_dense, &need);
+    if (need > 0 && (!workspace || workspace_bytes < need))
+        return fail(FP_ERR_VALUE, "workspace too small: need " + std::to_string(need) + " bytes");
+    DeviceGuard dg(P->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dev_info) CUDA_TRY(cudaMemsetAsync(dev_info, 0, sizeof(fp_solve_info), st));
+
+    void* cw = workspace;
+    void* rsb = out_dense ? out : (void*)((char*)workspace + cw_bytes(P));
+    double* mean_ws = P->mean_fix ? (double*)((char*)workspace + need - mean_bytes(P)) : nullptr;
+    const int plan_type = P->f32 ? ET_F32 : ET_F64;
+    const int plan_ctype = P->f32 ? ET_C64 : ET_C128;
+
+    auto buf_ptr = [&](int b) -> void* {
+        switch (b) {
+            case B_RHS: return const_cast<void*>(rhs);
+            case B_OUT: return out;
+            case B_RS: return rsb;
+            default: return cw;
+        }
+    };
+    auto buf_strides = [&](int b, int layout, long long s[3]) {
+        if (b == B_RHS) { for (int a = 0; a < 3; ++a) s[a] = rs_s[a]; return; }
+        if (b == B_OUT) { for (int a = 0; a < 3; ++a) s[a] = os_s[a]; return; }
+        if (b == B_RS) { for (int a = 0; a < 3; ++a) s[a] = out_dense ? os_s[a] : dense_r[a]; return; }
+        (void)layout;
+        for (int a = 0; a < 3; ++a) s[a] = cw_s[a];
+    };
+    auto buf_type = [&](int b, int layout) -> int {
+        if (layout == LY_CPLX) return plan_ctype;
+        if (b == B_RHS) return rhs_dtype == FP_F32 ? ET_F32 : ET_F64;
+        return plan_type;
+    };
+
+    cudaEvent_t* ev = (cudaEvent_t*)phase_events;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
+    int phase = 0;
+    bool first = true;
+    for (size_t i = 0; i < P->passes.size(); ++i) {
+        const PassT& T = P->passes[i];
+        while (ev && phase < T.phase) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
+        if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[i], st));
+        long long si[3], so[3];
+        buf_strides(T.in_buf, T.in_layout, si);
+        buf_strides(T.out_buf, T.out_layout, so);
+        Geometry g{};
+        if (T.engine != EN_SCALE) {
+            g.in = buf_ptr(T.in_buf);
+            g.out = buf_ptr(T.out_buf);
+            g.in_type = buf_type(T.in_buf, T.in_layout);
+            g.out_type = buf_type(T.out_buf, T.out_layout);
+            g.in_st = si[T.t];
+            g.out_st = so[T.t];
+            g.in_sa = T.a >= 0 ? si[T.a] : 0;
+            g.out_sa = T.a >= 0 ? so[T.a] : 0;
+            g.in_sb = T.b >= 0 ? si[T.b] : 0;
+            g.out_sb = T.b >= 0 ? so[T.b] : 0;
+        }
+        cudaError_t e = cudaSuccess;
+        if (T.engine == EN_FFT) {
+            FftPass p = T.fp;
+            g.na = p.g.na; g.nb = p.g.nb;
+            p.g = g;
+            p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
+            p.s.dc_out = dev_info ? &dev_info->dc : nullptr;
+            const size_t rb = P->f32 ? 4 : 8;
+            auto even_ok = [&](long long s, int ext) { return ext <= 1 || (s % 2) == 0; };
+            p.vec_in = (p.family == FAM_CONTIG) && g.in_st == 1 && (g.in_type == plan_type) &&
+                       even_ok(g.in_sa, g.na) && even_ok(g.in_sb, g.nb) &&
+                       ((uintptr_t)g.in % (2 * rb) == 0);
+            p.vec_out = (p.family == FAM_CONTIG) && g.out_st == 1 && (g.out_type == plan_type) &&
+                        even_ok(g.out_sa, g.na) && even_ok(g.out_sb, g.nb) &&
+                        ((uintptr_t)g.out % (2 * rb) == 0);
+            e = launch_fft_pass(p, P->f32, st);
+        } else if (T.engine == EN_DENSE) {
+            DensePass p = T.dp;
+            g.na = p.g.na; g.nb = p.g.nb;
+            p.g = g;
+            p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
+            e = launch_dense_pass(p, P->f32, st);
+        } else {
+            ScalePass p = T.sp;
+            const bool cpx = T.in_layout == LY_CPLX;
+            p.data = buf_ptr(T.in_buf);
+            p.type = cpx ? plan_ctype : plan_type;
+            // pad to 3 axes at the front
+            for (int k = 0; k < 3; ++k) { p.ext[k] = 1; p.st[k] = 0; }
+            for (int a = 0; a < d; ++a) {
+                p.ext[3 - d + a] = (int)(cpx ? P->cext[a] : P->n[a]);
+                p.st[3 - d + a] = si[a];
+            }
+            p.dc_out = dev_info ? &dev_info->dc : nullptr;
+            e = launch_scale_pass(p, P->f32, st);
+        }
+        if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+        first = false;
+    }
+    if (P->mean_fix) {
+        MeanPass m{};
+        for (int k = 0; k < 3; ++k) { m.ext[k] = 1; m.st[k] = 0; }
+        for (int a = 0; a < d; ++a) { m.ext[3 - d + a] = (int)P->n[a]; m.st[3 - d + a] = os_s[a]; }
+        m.data = out;
+        m.partials = mean_ws;
+        cudaError_t e = launch_mean_pass(m, P->f32, st);
+        if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("mean removal launch failed: ") + cudaGetErrorString(e));
+    }
+    if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[P->passes.size()], st));
+    while (ev && phase < 3) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
+    return FP_OK;
+}
+
+FP_API fp_status fp_removed_mean(const fp_plan* P, const fp_solve_info* h, double* rm) {
+    if (!P || !h || !rm) return fail(FP_ERR_VALUE, "NULL argument");
+    if (!P->singular) { *rm = 0.0; return FP_OK; }
+    // reference: Re(fftn(work)/prod n_p)[null] / _null_scale
+    *rm = (h->dc / P->np_prod) / P->null_scale;
+    return FP_OK;
+}
+
+FP_API fp_status fp_solve_host(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                               void* out, const int64_t* out_strides, fp_solve_result* result) {
+    if (!P || !rhs || !out) return fail(FP_ERR_VALUE, "NULL argument");
+    if (rhs_dtype != FP_F64 && rhs_dtype != FP_F32) return fail(FP_ERR_VALUE, "rhs dtype must be f64 or f32");
+    DeviceGuard dg(P->device);
+    const int d = P->ndim;
+    size_t cnt = 1;
+    for (int a = 0; a < d; ++a) cnt *= (size_t)P->n[a];
+    const size_t in_es = rhs_dtype == FP_F32 ? 4 : 8;
+    const size_t out_es = P->f32 ? 4 : 8;
+    long long dense_r[3];
+    dense_strides(P, false, dense_r);
+    // pack host arrays to dense C order (host-side gather for strided views)
+    auto is_dense = [&](const int64_t* s) {
+        if (!s) return true;
+        for (int a = 0; a < d; ++a) if (P->n[a] > 1 && s[a] != dense_r[a]) return false;
+        return true;
+    };
+    std::vector<unsigned char> in_pack, out_pack;
+    const unsigned char* hin = (const unsigned char*)rhs;
+    if (!is_dense(rhs_strides)) {
+        in_pack.resize(cnt * in_es);
+        size_t idx = 0;
+        for (long long i0 = 0; i0 < (d > 0 ? P->n[0] : 1); ++i0)
+            for (long long i1 = 0; i1 < (d > 1 ? P->n[1] : 1); ++i1)
+                for (long long i2 = 0; i2 < (d > 2 ? P->n[2] : 1); ++i2, ++idx) {
+                    long long off = i0 * rhs_strides[0] + (d > 1 ? i1 * rhs_strides[1] : 0) + (d > 2 ? i2 * rhs_strides[2] : 0);
+                    std::memcpy(&in_pack[idx * in_es], hin + off * in_es, in_es);
+                }
+        hin = in_pack.data();
+    }
+    cudaStream_t st;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaEvent_t ev[6];
+    for (int i = 0; i < 6; ++i) CUDA_TRY(cudaEventCreate(&ev[i]));
+    size_t ws = 0;
+    fp_plan_workspace_bytes(P, 1, &ws);
+    void *din = nullptr, *dout = nullptr, *dws = nullptr, *dinfo = nullptr;
+    fp_status rc = FP_OK;
+    fp_solve_info hinfo{};
+    CUDA_TRY(cudaEventRecord(ev[4], st));
+    if (cudaMallocAsync(&din, cnt * in_es, st) != cudaSuccess || cudaMallocAsync(&dout, cnt * out_es, st) != cudaSuccess ||
+        cudaMallocAsync(&dinfo, sizeof(fp_solve_info), st) != cudaSuccess ||
+        (ws && cudaMallocAsync(&dws, ws, st) != cudaSuccess)) {
+        rc = fail(FP_ERR_ALLOC, "device allocation failed");
+    }
+    if (rc == FP_OK && cudaMemcpyAsync(din, hin, cnt * in_es, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = fail(FP_ERR_CUDA, "H2D copy failed");
+    if (rc == FP_OK)
+        rc = fp_solve(P, din, rhs_dtype, nullptr, dout, nullptr, dws, ws, st, (fp_solve_info*)dinfo, (void* const*)ev);
+    if (rc == FP_OK && cudaMemcpyAsync(&hinfo, dinfo, sizeof(hinfo), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = fail(FP_ERR_CUDA, "D2H info copy failed");
+    if (rc == FP_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(FP_ERR_CUDA, "solve failed");
+    if (rc == FP_OK && hinfo.nonfinite) rc = fail(FP_ERR_NONFINITE, "rhs contains non-finite values");
+    if (rc == FP_OK) {
+        if (is_dense(out_strides)) {
+            if (cudaMemcpyAsync(out, dout, cnt * out_es, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = fail(FP_ERR_CUDA, "D2H copy failed");
+        } else {
+            out_pack.resize(cnt * out_es);
+            if (cudaMemcpyAsync(out_pack.data(), dout, cnt * out_es, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = fail(FP_ERR_CUDA, "D2H copy failed");
+        }
+    }
+    CUDA_TRY(cudaEventRecord(ev[5], st));
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == FP_OK) rc = fail(FP_ERR_CUDA, "D2H failed");
+    if (rc == FP_OK && !out_pack.empty()) {
+        unsigned char* hout = (unsigned char*)out;
+        size_t idx = 0;
+        for (long long i0 = 0; i0 < (d > 0 ? P->n[0] : 1); ++i0)
+            for (long long i1 = 0; i1 < (d > 1 ? P->n[1] : 1); ++i1)
+                for (long long i2 = 0; i2 < (d > 2 ? P->n[2] : 1); ++i2, ++idx) {
+                    long long off = i0 * out_strides[0] + (d > 1 ? i1 * out_strides[1] : 0) + (d > 2 ? i2 * out_strides[2] : 0);
+                    std::memcpy(hout + off * out_es, &out_pack[idx * out_es], out_es);
+                }
+    }
+    if (rc == FP_OK && result) {
+        float ms[4] = {0, 0, 0, 0};
+        cudaEventElapsedTime(&ms[0], ev[0], ev[1]);
+        cudaEventElapsedTime(&ms[1], ev[1], ev[2]);
+        cudaEventElapsedTime(&ms[2], ev[2], ev[3]);
+        cudaEventElapsedTime(&ms[3], ev[4], ev[5]);
+        for (int i = 0; i < 3; ++i) result->timing[i] = ms[i] * 1e-3;
+        result->total_seconds = ms[3] * 1e-3;
+        fp_removed_mean(P, &hinfo, &result->removed_mean);
+    }
+    if (din) cudaFreeAsync(din, st);
+    if (dout) cudaFreeAsync(dout, st);
+    if (dws) cudaFreeAsync(dws, st);
+    if (dinfo) cudaFreeAsync(dinfo, st);
+    cudaStreamSynchronize(st);
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(ev[i]);
+    cudaStreamDestroy(st);
+    return rc;
+}
+
+// ---------------------------------------------------------------------------
+// TransformPlan (transforms.py:128-177) on the device
+FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int device, fp_transform** out) {
+    if (!out) return fail(FP_ERR_VALUE, "NULL argument");
+    *out = nullptr;
+    if (kind < FP_DFT || kind > FP_DCT3) return fail(FP_ERR_VALUE, "unknown transform kind");
+    const long long min_len = kind == FP_DCT1 ? 2 : 1;
+    if (n < min_len) return fail(FP_ERR_CONFIG, "transform length too small");
+    if (precision != FP_F64 && precision != FP_F32) return fail(FP_ERR_VALUE, "precision must be f64 or f32");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(FP_ERR_CUDA, "no CUDA device available");
+    DeviceGuard dg(device);
+    fp_transform* T = new fp_transform();
+    T->device = device;
+    T->kind = kind;
+    T->n = n;
+    T->f32 = precision == FP_F32;
+    long long M = 0;
+    if (kind == FP_DFT || kind == FP_IDFT) M = n;
+    else if (kind == FP_DST2 || kind == FP_DST3 || kind == FP_DCT2 || kind == FP_DCT3) M = (n % 2 == 0) ? n / 2 : 0;
+    T->fft = M >= 16 && M <= 4096 && is_pow2(M);
+    fp_status st;
+    if (T->fft) {
+        T->M = (int)M;
+        std::vector<long double> wf, wt, ww;
+        fft_tables((int)n, (int)M, !(kind == FP_DFT || kind == FP_IDFT), wf, wt, ww);
+        if ((st = upload(T->allocs, wf, T->f32, &T->tab.wfft)) != FP_OK) { delete T; return st; }
+        if ((st = upload(T->allocs, wt, T->f32, &T->tab.wt)) != FP_OK) { delete T; return st; }
+        if ((st = upload(T->allocs, ww, T->f32, &T->tab.ww)) != FP_OK) { delete T; return st; }
+    } else {
+        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length needs the dense engine (n <= 4096)"); }
+        std::vector<long double> m;
+        int no, ni;
+        bool cpx;
+        dense_matrix(kind, (int)n, m, &no, &ni, &cpx);
+        T->tab.fwd_nout = no; T->tab.fwd_nin = ni; T->tab.fwd_cpx = cpx;
+        if ((st = upload(T->allocs, m, T->f32, &T->tab.mat_f)) != FP_OK) { delete T; return st; }
+    }
+    *out = T;
+    return FP_OK;
+}
+
+FP_API fp_status fp_transform_destroy(fp_transform* t) {
+    delete t;
+    return FP_OK;
+}
+
+FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int64_t* shape, int axis,
+                                      const void* in, int in_dtype, const int64_t* in_strides, void* out,
+                                      int out_dtype, const int64_t* out_strides, void* stream) {
+    if (!T || !shape || !in || !out || !in_strides || !out_strides) return fail(FP_ERR_VALUE, "NULL argument");
+    if (ndim < 1 || ndim > 3) return fail(FP_ERR_VALUE, "1 to 3 dimensions supported");
+    if (axis < 0 || axis >= ndim) return fail(FP_ERR_VALUE, "axis out of range");
+    if (shape[axis] != T->n) return fail(FP_ERR_VALUE, "plan length does not match the array along axis");
+    const bool cpx_kind = T->kind == FP_DFT || T->kind == FP_IDFT;
+    const bool out_c = out_dtype == FP_C128 || out_dtype == FP_C64;
+    if (cpx_kind != out_c) return fail(FP_ERR_VALUE, "output dtype does not match the transform kind");
+    if (!cpx_kind && (in_dtype == FP_C128 || in_dtype == FP_C64)) return fail(FP_ERR_VALUE, "real transform of complex data");
+    DeviceGuard dg(T->device);
+    int o[2] = {-1, -1}, k = 0;
+    for (int a = 0; a < ndim; ++a) if (a != axis) o[k++] = a;
+    int aa = -1, bb = -1;
+    if (k == 2) { aa = o[0]; bb = o[1]; } else if (k == 1) { bb = o[0]; }
+    Geometry g{};
+    g.na = aa >= 0 ? (int)shape[aa] : 1;
+    g.nb = bb >= 0 ? (int)shape[bb] : 1;
+    g.in = in; g.out = out;
+    g.in_type = in_dtype; g.out_type = out_dtype;
+    g.in_st = in_strides[axis]; g.out_st = out_strides[axis];
+    g.in_sa = aa >= 0 ? in_strides[aa] : 0; g.out_sa = aa >= 0 ? out_strides[aa] : 0;
+    g.in_sb = bb >= 0 ? in_strides[bb] : 0; g.out_sb = bb >= 0 ? out_strides[bb] : 0;
+    const double om = (T->kind == FP_DFT) ? 1.0 / (double)T->n : 1.0;
+    cudaError_t e;
+    if ((long long)g.na * g.nb == 0) return FP_OK;
+    if (T->fft) {
+        FftPass p{};
+        const bool inv = T->kind == FP_IDFT || T->kind == FP_DST3 || T->kind == FP_DCT3;
+        p.op = inv ? OP_INV : OP_FWD;
+        p.fkind = T->kind == FP_DFT ? FK_CFFT : (T->kind == FP_DST2 ? FK_DST2 : FK_DCT2);
+        p.ikind = T->kind == FP_IDFT ? IK_ICFFT : (T->kind == FP_DST3 ? IK_DST3 : IK_DCT3);
+        p.family = (axis == ndim - 1) ? FAM_CONTIG : FAM_STRIDED;
+        p.n = (int)T->n;
+        p.M = T->M;
+        p.logM = ilog2(T->M);
+        p.ls = p.M + p.M / 16 + 1;
+        if ((p.ls & 1) == 0) p.ls += 1;
+        const bool in_c = in_dtype == FP_C128 || in_dtype == FP_C64;
+        fft_tile_shape(p, T->f32, in_c || cpx_kind, g.na, g.nb);
+        p.g = g;
+        p.wfft = T->tab.wfft; p.wt = T->tab.wt; p.ww = T->tab.ww;
+        p.out_mult = om;
+        p.vec_in = 0; p.vec_out = 0;
+        p.nonfinite = nullptr;
+        p.s = Scaling{};
+        e = launch_fft_pass(p, T->f32, (cudaStream_t)stream);
+    } else {
+        DensePass p{};
+        const bool in_c = in_dtype == FP_C128 || in_dtype == FP_C64;
+        p.cls = cpx_kind ? DC_C2C : DC_R2R;
+        p.n_in = T->tab.fwd_nin; p.n_out = T->tab.fwd_nout;
+        p.mat = T->tab.mat_f;
+        p.g = g;
+        if (cpx_kind && !in_c) {
+            // real data into the complex dense transform: the kernel widens on load
+            p.cls = DC_C2C;
+        }
+        p.in_ls = (p.cls == DC_R2R) ? p.n_in : 2 * p.n_in;
+        const int rb = T->f32 ? 4 : 8;
+        int lines = std::max(1, (48 * 1024) / (p.in_ls * rb));
+        lines = std::min(lines, 64);
+        const long long nl = (long long)g.na * g.nb;
+        if (lines > nl) lines = (int)nl;
+        p.lines = lines;
+        p.tiles = (int)((nl + lines - 1) / lines);
+        p.out_mult = om;
+        p.nonfinite = nullptr;
+        e = launch_dense_pass(p, T->f32, (cudaStream_t)stream);
+    }
+    if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
+    return FP_OK;
+}
+
+FP_API fp_status fp_event_create(void** event) {
+    if (!event) return fail(FP_ERR_VALUE, "NULL argument");
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    *event = (void*)e;
+    return FP_OK;
+}
+
+FP_API fp_status fp_event_destroy(void* event) {
+    if (event) CUDA_TRY(cudaEventDestroy((cudaEvent_t)event));
+    return FP_OK;
+}
+
+FP_API fp_status fp_event_elapsed_ms(void* start, void* stop, float* ms) {
+    if (!start || !stop || !ms) return fail(FP_ERR_VALUE, "NULL argument");
+    CUDA_TRY(cudaEventSynchronize((cudaEvent_t)stop));
+    CUDA_TRY(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+    return FP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,22 @@
+// fp_tables.h -- plan-time host tables (see fp_tables.cpp)
+#pragma once
+#include <vector>
+
+namespace fpb {
+
+struct AxisSpec {
+    long long n;
+    double length;
+    int bc;    // FP_BC_*
+    int kind;  // FP_GRID_*
+};
+
+void exact_cis(long long num, long long den, long double* c, long double* s);
+void fft_tables(int n_real, int M, bool real_kind, std::vector<long double>& wfft,
+                std::vector<long double>& wt, std::vector<long double>& ww);
+double axis_dx(const AxisSpec& a);
+std::vector<double> eigenvalue_table(const AxisSpec& a, int approx);
+// kind: FP_DFT..FP_DCT3, or 100 (real-input DFT half spectrum), 101 (half spectrum -> real)
+bool dense_matrix(int kind, int n, std::vector<long double>& m, int* n_out, int* n_in, bool* cpx);
+
+}  // namespace fpb

@@ -1,0 +1,111 @@
+// fp_types.h -- pass descriptors shared by the host planner (fp_plan.cu) and
+// the sm_100a kernels (fp_kernels.cu).
+//
+// One Poisson solve is a short list of PASSES over HBM.  A pass transforms
+// every line along one axis `t` of a (up to) 3D array; the lines are indexed by
+// the two other axes `a` (outer) and `b` (inner).  Three pass ops exist:
+//   FWD  forward 1D transform            (solver.py:234-240 for one axis)
+//   INV  inverse 1D transform            (solver.py:242-249 for one axis)
+//   MID  forward -> eigenvalue scale -> inverse along the last forward axis,
+//        with null-mode capture (solver.py:216-223), all on one on-chip tile.
+#pragma once
+#include <stdint.h>
+
+namespace fpb {
+
+enum PassOp { OP_FWD = 0, OP_INV = 1, OP_MID = 2 };
+
+// Forward / inverse line kinds of the FFT engine (power-of-two lengths).
+// DCT2/DST2/RFFT are real-to-real/-complex transforms built around a
+// half-length complex FFT (Makhoul reordering + real-FFT untangling).
+enum FwdKind { FK_DCT2 = 0, FK_DST2 = 1, FK_RFFT = 2, FK_CFFT = 3 };
+enum InvKind { IK_DCT3 = 0, IK_DST3 = 1, IK_IRFFT = 2, IK_ICFFT = 3 };
+
+// Dense (direct-summation) engine classes, any length, any kind.
+enum DenseClass { DC_R2R = 0, DC_R2C = 1, DC_C2C = 2, DC_C2R = 3 };
+
+// Line-to-thread family: CONTIG = lines are contiguous rows (transform axis is
+// the unit-stride axis); STRIDED = lines are columns, W adjacent columns per
+// tile so every row segment is a coalesced run.
+enum Family { FAM_CONTIG = 0, FAM_STRIDED = 1 };
+
+// element types (match FP_F64.. in the public header)
+enum ElemType { ET_F64 = 0, ET_F32 = 1, ET_C128 = 2, ET_C64 = 3 };
+
+struct Geometry {
+    int na, nb;                 // extents of the line-index axes (a outer, b inner)
+    long long in_st, in_sa, in_sb;    // strides (elements of in_type)
+    long long out_st, out_sa, out_sb; // strides (elements of out_type)
+    const void* in;
+    void* out;
+    int in_type, out_type;
+};
+
+// Eigenvalue scaling of the middle pass (solver.py:151-159,221).  The factor
+// for spectral index (k_t, k_a, k_b) is  bscale / lam  with
+// lam = sum over axes in AXIS ORDER of the per-axis tables (eigenvalues.py:104-108),
+// and 0 where lam == 0 (the null mode, solver.py:157-158).
+struct Scaling {
+    const double* lam_t;        // table along the transform axis (n_t entries)
+    const double* lam_a;        // table along axis a (nullptr => 0)
+    const double* lam_b;        // table along axis b (nullptr => 0)
+    int pos_t, pos_a, pos_b;    // axis ids (summation order); -1 = absent axis
+    double bscale;              // prod backward_scale (transforms.py:88-96)
+    double inv_np;              // 1 / prod n_periodic (solver.py:238-239)
+    int singular;
+    double* dc_out;             // raw null-mode coefficient sink (or nullptr)
+};
+
+struct FftPass {
+    int op, fkind, ikind, family;
+    int n;                      // real line length (or complex length for CFFT)
+    int M, logM;                // complex FFT length
+    int lines;                  // lines per tile (W for STRIDED; pow2)
+    int logLines;
+    int ls;                     // shared-memory line stride in complex elements
+    int tiles;                  // grid size
+    int nbt;                    // STRIDED: tiles along b
+    int vec_in, vec_out;        // 16-byte vector path allowed (contiguous pairs)
+    Geometry g;
+    Scaling s;
+    const void* wfft;           // M roots  e^{-2 pi i k/M}          (Real2)
+    const void* wt;             // M+1 roots e^{-2 pi i k/n}  (real kinds)
+    const void* ww;             // M+1 roots e^{-i pi k/(2n)} (DCT/DST)
+    int* nonfinite;             // first pass only
+    double out_mult;            // extra output scale (DFT 1/n in TransformPlan)
+};
+
+struct DensePass {
+    int cls;                    // DenseClass
+    int n_in, n_out;
+    int lines;                  // lines per CTA
+    int tiles;
+    int in_ls, out_ls;          // smem line strides (reals)
+    Geometry g;
+    const void* mat;            // [n_out][n_in] Real (R2R) or Real2 (others)
+    int* nonfinite;
+    double out_mult;
+};
+
+struct ScalePass {              // stand-alone eigenvalue scale (dense middle)
+    int ndim;
+    int ext[3];                 // spectral extents
+    long long st[3];            // strides (elements)
+    void* data;
+    int type;
+    const double* lam[3];
+    double bscale;
+    double inv_np;
+    int singular;
+    double* dc_out;
+};
+
+struct MeanPass {               // subtract the arithmetic mean (DCT-I plans)
+    int ext[3];
+    long long st[3];
+    void* data;                 // real, plan precision
+    double* partials;           // kMeanParts + 1 doubles of workspace
+};
+constexpr int kMeanParts = 1184;  // 8 x 148 SMs
+
+}  // namespace fpb
