@@ -171,6 +171,31 @@ def cpu_baseline_sample(name, seconds_cap=30.0):
                       "algorithm (scipy.fft, workers=all cores) on this box's host"}
 
 
+def measure_e2e(plan, rhs, shape, tdt, n_pts, s, args, ws, dist, dev):
+    """Same metric through the public API with pinned host buffers (H2D + solve + D2H per step)."""
+    import torch
+
+    rhs_host = torch.empty(shape, dtype=tdt, pin_memory=True)
+    rhs_host.copy_(rhs)
+    out_host = torch.empty(shape, dtype=tdt, pin_memory=True)
+    rhs_np, out_np = rhs_host.numpy(), out_host.numpy()
+    plan.solve(rhs_np, out=out_np)  # warm the path
+    e2e_steps = max(1, min(args.steps, 10))
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.solve(rhs_np, out=out_np)
+    e2e_dt = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_dt = float(tt.item())
+    e2e = {"value": ws * e2e_steps / e2e_dt, "unit": "solves/s", "h2d_bytes_per_step": n_pts * s,
+           "d2h_bytes_per_step": n_pts * s + 16, "path": "SolverPlan.solve(numpy pinned rhs, out=numpy pinned)"}
+    return e2e
+
+
 def run_ours(args, ws, rank, local):
     import ctypes
 
@@ -287,24 +312,9 @@ def run_ours(args, ws, rank, local):
                   "frac": b_alg / (ms_step * 1e-3) / 1e9 / hbm_peak},
     }
     # e2e through the public API with pinned host buffers (H2D + solve + D2H each step)
-    rhs_host = torch.empty(shape, dtype=tdt, pin_memory=True)
-    rhs_host.copy_(rhs)
-    out_host = torch.empty(shape, dtype=tdt, pin_memory=True)
-    rhs_np, out_np = rhs_host.numpy(), out_host.numpy()
-    plan.solve(rhs_np, out=out_np)  # warm the path
-    e2e_steps = max(1, min(args.steps, 10))
-    if dist is not None:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        plan.solve(rhs_np, out=out_np)
-    e2e_dt = time.perf_counter() - t0
-    if dist is not None:
-        tt = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_dt = float(tt.item())
-    e2e = {"value": ws * e2e_steps / e2e_dt, "unit": "solves/s", "h2d_bytes_per_step": n_pts * s,
-           "d2h_bytes_per_step": n_pts * s + 16, "path": "SolverPlan.solve(numpy pinned rhs, out=numpy pinned)"}
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(plan, rhs, shape, tdt, n_pts, s, args, ws, dist, dev)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args.config)
@@ -337,6 +347,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_env()

@@ -18,20 +18,14 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB_PATH = LIB_DIR / "libfastpoisson_b200.so"
 
-SOURCES = ["fp_kernels.cu", "fp_plan.cu", "fp_tables.cpp"]
-HEADERS = ["fp_types.h", "fp_tables.h"]
+SOURCES = ["fp_fft_d_hi.cu", "fp_fft_d_lo.cu", "fp_fft_f_hi.cu", "fp_fft_f_lo.cu",
+           "fp_kernels.cu", "fp_plan.cu", "fp_tables.cpp"]
+HEADERS = ["fp_types.h", "fp_tables.h", "fp_common.cuh", "fp_fft.cuh"]
+OBJ_DIR = PKG / "build"
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = [
-    "-O3",
-    "-lineinfo",
-    "-std=c++17",
-    "-Xcompiler",
-    "-fPIC,-fvisibility=hidden",
-    "-shared",
-    "-cudart",
-    "static",
-]
+COMPILE_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden"]
+LINK_FLAGS = ["-shared", "-cudart", "static"]
 
 
 def nvcc_path() -> str:
@@ -55,18 +49,36 @@ def is_stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the library if missing or older than its sources."""
+    """Compile the library if missing or older than its sources (one nvcc per
+    translation unit, in parallel, then one link)."""
     if not force and not is_stale():
         return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
+
     LIB_DIR.mkdir(parents=True, exist_ok=True)
+    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    nvcc = nvcc_path()
+
+    def compile_one(src):
+        obj = OBJ_DIR / (src + ".o")
+        cmd = [nvcc, *ARCH_FLAGS, *COMPILE_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        proc = subprocess.run(cmd, capture_output=True, text=True)
+        if proc.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src} ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
+        return obj
+
+    workers = max(1, min(len(SOURCES), os.cpu_count() or 1))
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, "-o", str(tmp)]
-    cmd += [str(CSRC / s) for s in SOURCES]
+    cmd = [nvcc, *ARCH_FLAGS, *LINK_FLAGS, "-o", str(tmp), *map(str, objs)]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
+        raise RuntimeError(f"nvcc link failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -1,0 +1,229 @@
+// fp_common.cuh -- device building blocks shared by the sm_100a kernels:
+// complex arithmetic, in-register DFTs, compile-time Stockham stages, the
+// real-FFT untangle/tangle, typed loads/stores, per-line tile bookkeeping.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "fp_types.h"
+
+namespace fpb {
+
+// ----------------------------------------------------------------------------
+// complex helpers
+template <typename T> struct CxOf;
+template <> struct CxOf<double> { using type = double2; };
+template <> struct CxOf<float> { using type = float2; };
+template <typename T> using cx = typename CxOf<T>::type;
+
+template <typename T> __device__ __forceinline__ cx<T> mkc(T a, T b) { cx<T> r; r.x = a; r.y = b; return r; }
+template <typename T> __device__ __forceinline__ cx<T> cadd(cx<T> a, cx<T> b) { return mkc<T>(a.x + b.x, a.y + b.y); }
+template <typename T> __device__ __forceinline__ cx<T> csub(cx<T> a, cx<T> b) { return mkc<T>(a.x - b.x, a.y - b.y); }
+template <typename T> __device__ __forceinline__ cx<T> cmul(cx<T> a, cx<T> b) {
+    return mkc<T>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename T> __device__ __forceinline__ cx<T> cmulc(cx<T> a, cx<T> b) {
+    return mkc<T>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename T> __device__ __forceinline__ cx<T> cscale(cx<T> a, T s) { return mkc<T>(a.x * s, a.y * s); }
+
+// padded shared-memory index: one pad slot per 16 complex elements keeps the
+// Stockham scatter (stride R) and the column accesses bank-conflict free.
+__device__ __forceinline__ int P(int i) { return i + (i >> 4); }
+// padded index for the real-valued view used by the DCT-III/DST-III loads
+__device__ __forceinline__ int PR(int i) { return i + (i >> 5); }
+
+// ----------------------------------------------------------------------------
+// in-register DFT of size R (2,4,8,16), natural order in and out.
+// 16th roots of unity, correctly rounded.
+__device__ __forceinline__ double c16(int m) {
+    switch (m & 15) {
+        case 0: return 1.0;
+        case 1: return 0.92387953251128673848259;
+        case 2: return 0.70710678118654752440084;
+        case 3: return 0.38268343236508977172846;
+        case 4: return 0.0;
+        case 5: return -0.38268343236508977172846;
+        case 6: return -0.70710678118654752440084;
+        case 7: return -0.92387953251128673848259;
+        case 8: return -1.0;
+        case 9: return -0.92387953251128673848259;
+        case 10: return -0.70710678118654752440084;
+        case 11: return -0.38268343236508977172846;
+        case 12: return 0.0;
+        case 13: return 0.38268343236508977172846;
+        case 14: return 0.70710678118654752440084;
+        default: return 0.92387953251128673848259;
+    }
+}
+__device__ __forceinline__ double s16(int m) { return c16(m - 4); }  // sin(2 pi m/16)
+
+// multiply by w = e^{-+2 pi i m/16} (forward: minus); m is a compile-time constant after unrolling
+template <bool INV, typename T>
+__device__ __forceinline__ cx<T> rot16(cx<T> c, int m) {
+    if (m == 0) return c;
+    if (m == 4) return INV ? mkc<T>(-c.y, c.x) : mkc<T>(c.y, -c.x);
+    const T wr = (T)c16(m);
+    const T wi = INV ? (T)s16(m) : (T)(-s16(m));
+    return mkc<T>(c.x * wr - c.y * wi, c.x * wi + c.y * wr);
+}
+
+template <int R> __device__ __forceinline__ constexpr int brev(int i) {
+    return R == 2 ? i
+         : R == 4 ? (((i & 1) << 1) | ((i >> 1) & 1))
+         : R == 8 ? (((i & 1) << 2) | (i & 2) | ((i >> 2) & 1))
+                  : (((i & 1) << 3) | ((i & 2) << 1) | ((i >> 1) & 2) | ((i >> 3) & 1));
+}
+
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void dft_reg(cx<T>* v) {
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int j = brev<R>(i);
+        if (j > i) { cx<T> t = v[i]; v[i] = v[j]; v[j] = t; }
+    }
+#pragma unroll
+    for (int s = 2; s <= R; s *= 2) {
+        const int h = s / 2;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+            const int m = k * (16 / s);
+#pragma unroll
+            for (int b = 0; b < R; b += s) {
+                const cx<T> a = v[b + k];
+                const cx<T> c = rot16<INV, T>(v[b + k + h], m);
+                v[b + k] = cadd<T>(a, c);
+                v[b + k + h] = csub<T>(a, c);
+            }
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// one Stockham stage of radix R over every line of the tile (in place, two
+// barriers).  Compile-time M, R and Ns: every shared-memory address is the
+// thread's base plus a constant.  Thread -> (line, jt); 16/R butterflies each.
+template <int R> struct LogR { static constexpr int v = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4; };
+
+template <int R, int LOGNS, bool INV, typename T, int LOGM>
+__device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+    constexpr int M = 1 << LOGM;
+    constexpr int LOGR = LogR<R>::v;
+    constexpr int NB = 16 / R;
+    constexpr int TL = M / 16;
+    constexpr int NS = 1 << LOGNS;
+    constexpr int STRIDE_IN = M >> LOGR;
+    cx<T> v[16];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = jt + b * TL;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b * R + r] = line[P(j + r * STRIDE_IN)];
+        if (LOGNS > 0) {
+            const int e = (j & (NS - 1)) << (LOGM - LOGNS - LOGR);
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const cx<T> w = __ldg(&W[(r * e) & (M - 1)]);
+                v[b * R + r] = INV ? cmulc<T>(v[b * R + r], w) : cmul<T>(v[b * R + r], w);
+            }
+        }
+        dft_reg<R, INV, T>(v + b * R);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int j = jt + b * TL;
+        const int base = ((j >> LOGNS) << (LOGNS + LOGR)) + (j & (NS - 1));
+#pragma unroll
+        for (int r = 0; r < R; ++r) line[P(base + r * NS)] = v[b * R + r];
+    }
+    __syncthreads();
+}
+
+template <int LOGNS, bool INV, typename T, int LOGM>
+__device__ __forceinline__ void radix16_stages(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+    if constexpr (LOGNS < LOGM) {
+        stockham_stage<16, LOGNS, INV, T, LOGM>(line, jt, W);
+        radix16_stages<LOGNS + 4, INV, T, LOGM>(line, jt, W);
+    }
+}
+
+template <bool INV, typename T, int LOGM>
+__device__ __forceinline__ void fft_tile(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+    constexpr int REM = LOGM & 3;
+    if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM>(line, jt, W);
+    if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
+    if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
+    radix16_stages<REM, INV, T, LOGM>(line, jt, W);
+}
+
+// ----------------------------------------------------------------------------
+// real-FFT untangle / tangle (half-length trick)
+// split: V_k = 1/2 (Z_k + conj Z_{M-k}) - 1/2 i t_k (Z_k - conj Z_{M-k}),  t_k = e^{-2 pi i k/n}
+template <typename T>
+__device__ __forceinline__ cx<T> rsplit(cx<T> zk, cx<T> zm, cx<T> tk) {
+    const cx<T> A = mkc<T>(zk.x + zm.x, zk.y - zm.y);
+    const cx<T> B = mkc<T>(zk.x - zm.x, zk.y + zm.y);
+    const cx<T> tB = cmul<T>(tk, B);
+    return mkc<T>((T)0.5 * (A.x + tB.y), (T)0.5 * (A.y - tB.x));
+}
+// merge: Z_k = (V_k + conj V_{M-k}) + i conj(t_k) (V_k - conj V_{M-k})
+template <typename T>
+__device__ __forceinline__ cx<T> rmerge(cx<T> vk, cx<T> vm, cx<T> tk) {
+    const cx<T> A = mkc<T>(vk.x + vm.x, vk.y - vm.y);
+    const cx<T> B = mkc<T>(vk.x - vm.x, vk.y + vm.y);
+    const cx<T> cB = cmulc<T>(B, tk);  // B * conj(t)
+    return mkc<T>(A.x - cB.y, A.y + cB.x);
+}
+
+// ----------------------------------------------------------------------------
+// typed global loads / stores with conversion
+template <typename T>
+__device__ __forceinline__ T ld_real(const void* p, int type, long long off) {
+    if (type == ET_F32) return (T)__ldg(reinterpret_cast<const float*>(p) + off);
+    return (T)__ldg(reinterpret_cast<const double*>(p) + off);
+}
+template <typename T>
+__device__ __forceinline__ cx<T> ld_cx(const void* p, int type, long long off) {
+    if (type == ET_C64) { const float2 v = __ldg(reinterpret_cast<const float2*>(p) + off); return mkc<T>((T)v.x, (T)v.y); }
+    if (type == ET_C128) { const double2 v = __ldg(reinterpret_cast<const double2*>(p) + off); return mkc<T>((T)v.x, (T)v.y); }
+    return mkc<T>(ld_real<T>(p, type, off), (T)0);  // real input into a complex transform
+}
+template <typename T>
+__device__ __forceinline__ void st_real(void* p, int type, long long off, T v) {
+    if (type == ET_F32) reinterpret_cast<float*>(p)[off] = (float)v;
+    else reinterpret_cast<double*>(p)[off] = (double)v;
+}
+template <typename T>
+__device__ __forceinline__ void st_cx(void* p, int type, long long off, cx<T> v) {
+    if (type == ET_C64) reinterpret_cast<float2*>(p)[off] = make_float2((float)v.x, (float)v.y);
+    else reinterpret_cast<double2*>(p)[off] = make_double2((double)v.x, (double)v.y);
+}
+
+template <typename T> __device__ __forceinline__ bool finite_t(T x) { return isfinite(x); }
+
+// per-line bookkeeping of a tile
+struct LineInfo {
+    long long in_off, out_off;
+    double before, after1, after2;  // eigenvalue partial sums (axis order)
+    int nafter, valid, null_line, pad;
+};
+// the line table is padded so the complex tile behind it is 16-byte aligned
+__host__ __device__ __forceinline__ size_t linfo_bytes(int lines) {
+    return (sizeof(LineInfo) * (size_t)lines + 15) & ~(size_t)15;
+}
+
+// eigenvalue factor for transform-axis index kt on line `L`
+template <typename T>
+__device__ __forceinline__ T eig_factor(const Scaling& s, const LineInfo& L, int kt) {
+    double lam = L.before + __ldg(&s.lam_t[kt]);
+    if (L.nafter > 0) lam += L.after1;
+    if (L.nafter > 1) lam += L.after2;
+    double f = 0.0;
+    if (lam != 0.0) f = (s.bscale / lam) * s.inv_np;
+    return (T)f;
+}
+
+// ----------------------------------------------------------------------------
+
+}  // namespace fpb

@@ -268,7 +268,7 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
         while (lines > 1 && lines / 2 >= nb) lines /= 2;
         p.lines = lines;
         p.logLines = ilog2(lines);
-        while (p.lines > 1 && ((p.lines << logTL) > (f32 ? 1024 : 512) || fft_pass_smem_bytes(p, real_bytes) > 200 * 1024)) {
+        while (p.lines > 1 && ((p.lines << logTL) > 512 || fft_pass_smem_bytes(p, real_bytes) > 200 * 1024)) {
             p.lines /= 2;
             p.logLines -= 1;
         }
