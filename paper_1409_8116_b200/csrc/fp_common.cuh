@@ -105,8 +105,23 @@ __device__ __forceinline__ void dft_reg(cx<T>* v) {
 // thread's base plus a constant.  Thread -> (line, jt); 16/R butterflies each.
 template <int R> struct LogR { static constexpr int v = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4; };
 
+// Per-stage twiddle tables: stage (R, Ns) of an M-point FFT multiplies input r
+// of butterfly j by W_M^{r (j mod Ns) M/(Ns R)}.  The host stores, for every
+// stage with Ns > 1, a table tw[r][e] (r < R, e < Ns) -- r-major, so the lanes
+// of a warp (consecutive e) read consecutive entries: coalesced, L1-resident,
+// and no fp64 work for the twiddles.  Offsets of the stages are compile-time.
+__host__ __device__ constexpr int stage_tw_offset(int logM, int logNs) {
+    // stages with Ns > 1 are the radix-16 stages at LOGNS = rem, rem+4, ... (rem = logM & 3),
+    // plus LOGNS = 4 when rem == 0; each holds 16 * Ns entries
+    int off = 0;
+    int l = (logM & 3) ? (logM & 3) : 4;
+    while (l < logNs) { off += 16 << l; l += 4; }
+    return off;
+}
+__host__ __device__ constexpr int stage_tw_total(int logM) { return stage_tw_offset(logM, logM); }
+
 template <int R, int LOGNS, bool INV, typename T, int LOGM>
-__device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+__device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* __restrict__ W) {
     constexpr int M = 1 << LOGM;
     constexpr int LOGR = LogR<R>::v;
     constexpr int NB = 16 / R;
@@ -120,10 +135,10 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const cx<T>*
 #pragma unroll
         for (int r = 0; r < R; ++r) v[b * R + r] = line[P(j + r * STRIDE_IN)];
         if (LOGNS > 0) {
-            const int e = (j & (NS - 1)) << (LOGM - LOGNS - LOGR);
+            const cx<T>* tw = reinterpret_cast<const cx<T>*>(W) + stage_tw_offset(LOGM, LOGNS) + (j & (NS - 1));
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const cx<T> w = __ldg(&W[(r * e) & (M - 1)]);
+                const cx<T> w = __ldg(&tw[r * NS]);
                 v[b * R + r] = INV ? cmulc<T>(v[b * R + r], w) : cmul<T>(v[b * R + r], w);
             }
         }
@@ -141,7 +156,7 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const cx<T>*
 }
 
 template <int LOGNS, bool INV, typename T, int LOGM>
-__device__ __forceinline__ void radix16_stages(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+__device__ __forceinline__ void radix16_stages(cx<T>* line, int jt, const void* __restrict__ W) {
     if constexpr (LOGNS < LOGM) {
         stockham_stage<16, LOGNS, INV, T, LOGM>(line, jt, W);
         radix16_stages<LOGNS + 4, INV, T, LOGM>(line, jt, W);
@@ -149,12 +164,21 @@ __device__ __forceinline__ void radix16_stages(cx<T>* line, int jt, const cx<T>*
 }
 
 template <bool INV, typename T, int LOGM>
-__device__ __forceinline__ void fft_tile(cx<T>* line, int jt, const cx<T>* __restrict__ W) {
+__device__ __forceinline__ void fft_tile(cx<T>* line, int jt, const void* __restrict__ W) {
     constexpr int REM = LOGM & 3;
     if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
     radix16_stages<REM, INV, T, LOGM>(line, jt, W);
+}
+
+// twiddles of the mirrored index M-q from those of q (n = 2M):
+//   t_{M-q} = e^{-2 pi i (M-q)/n} = -conj(t_q)
+//   w_{M-q} = e^{-i pi (M-q)/(2n)} = e^{-i pi/4} conj(w_q)
+template <typename T> __device__ __forceinline__ cx<T> t_mirror(cx<T> t) { return mkc<T>(-t.x, t.y); }
+template <typename T> __device__ __forceinline__ cx<T> w_mirror(cx<T> w) {
+    const T c = (T)0.70710678118654752440084;
+    return mkc<T>(c * (w.x - w.y), -c * (w.x + w.y));
 }
 
 // ----------------------------------------------------------------------------
@@ -219,8 +243,15 @@ __device__ __forceinline__ T eig_factor(const Scaling& s, const LineInfo& L, int
     double lam = L.before + __ldg(&s.lam_t[kt]);
     if (L.nafter > 0) lam += L.after1;
     if (L.nafter > 1) lam += L.after2;
-    double f = 0.0;
-    if (lam != 0.0) f = (s.bscale / lam) * s.inv_np;
+    // bscale / lam via rcp.approx + two Newton steps (within 1 ulp of the IEEE
+    // quotient of solver.py:158); the null mode (lam == 0) maps to 0
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
+    double e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    const double f = lam != 0.0 ? (s.bscale * r) * s.inv_np : 0.0;
     return (T)f;
 }
 

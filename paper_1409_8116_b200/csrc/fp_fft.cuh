@@ -18,7 +18,7 @@ using FftKernelFn = void (*)(const FftPass);
 // Every per-thread loop has a compile-time trip count, and all of a thread's
 // global loads are issued before the first shared-memory store.
 
-template <typename T, int LOGM, bool STRIDED>
+template <typename T, int LOGM, bool STRIDED, int OP>
 __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int M = 1 << LOGM;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
     const int n = p.n;
-    const cx<T>* __restrict__ W = reinterpret_cast<const cx<T>*>(p.wfft);
+    const void* __restrict__ W = p.wfft;
     const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
     const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
     const Geometry& g = p.g;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
         L.null_line = (ia == 0 && ib == 0);
         double before = 0.0, a1 = 0.0, a2 = 0.0;
         int nafter = 0;
-        if (p.op == OP_MID) {
+        if (OP == OP_MID) {
             const bool ha = p.s.lam_a != nullptr, hb = p.s.lam_b != nullptr;
             const double la = ha ? p.s.lam_a[ia] : 0.0;
             const double lb = hb ? p.s.lam_b[ib] : 0.0;
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     cx<T>* line_io = sm + lio * LS;
     T* zr_io = reinterpret_cast<T*>(line_io);
     const LineInfo Lio = linfo[lio];
-    const bool fwd_in = p.op != OP_INV;
+    constexpr bool fwd_in = OP != OP_INV;
     bool bad = false;
 
     // =============== LOAD (batched: 16 complex / 32 real values per thread in flight)
@@ -211,10 +211,10 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     __syncthreads();
 
     // =============== FORWARD FFT (+ post / mid)
-    if (fwd_in) {
+    if constexpr (fwd_in) {
         fft_tile<false, T, LOGM>(line_f, jt, W);
 
-        if (p.op == OP_FWD) {
+        if constexpr (OP == OP_FWD) {
             const int kind = p.fkind;
             const T om = (T)p.out_mult;
             if (!Lio.valid) return;
@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                         st_cx<T>(g.out, g.out_type, ob + (long long)HALF * os, cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), om));
                     } else {
                         const cx<T> zk = line_io[P(q)], zm = line_io[P(M - q)];
-                        st_cx<T>(g.out, g.out_type, ob + (long long)q * os, cscale<T>(rsplit<T>(zk, zm, Wt[q]), om));
-                        st_cx<T>(g.out, g.out_type, ob + (long long)(M - q) * os, cscale<T>(rsplit<T>(zm, zk, Wt[M - q]), om));
+                        const cx<T> tq = Wt[q];
+                        st_cx<T>(g.out, g.out_type, ob + (long long)q * os, cscale<T>(rsplit<T>(zk, zm, tq), om));
+                        st_cx<T>(g.out, g.out_type, ob + (long long)(M - q) * os, cscale<T>(rsplit<T>(zm, zk, t_mirror<T>(tq)), om));
                     }
                 }
             } else {
@@ -259,8 +260,9 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                         EMIT(n - HALF, (T)-2 * U.y);
                     } else {
                         const cx<T> zk = line_io[P(q)], zm = line_io[P(M - q)];
-                        const cx<T> U1 = cmul<T>(Ww[q], rsplit<T>(zk, zm, Wt[q]));
-                        const cx<T> U2 = cmul<T>(Ww[M - q], rsplit<T>(zm, zk, Wt[M - q]));
+                        const cx<T> tq = Wt[q], wq = Ww[q];
+                        const cx<T> U1 = cmul<T>(wq, rsplit<T>(zk, zm, tq));
+                        const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit<T>(zm, zk, t_mirror<T>(tq)));
                         EMIT(q, (T)2 * U1.x);
                         EMIT(n - q, (T)-2 * U1.y);
                         EMIT(M - q, (T)2 * U2.x);
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                         line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
                     } else {
                         const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                        const cx<T> tq = Wt[q], tm = Wt[M - q];
+                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
                         const cx<T> xk = cscale<T>(rsplit<T>(zk, zm, tq), eig_factor<T>(S, L, q));
                         const cx<T> xm = cscale<T>(rsplit<T>(zm, zk, tm), eig_factor<T>(S, L, M - q));
                         line_f[P(q)] = rmerge<T>(xk, xm, tq);
@@ -334,8 +336,8 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                         line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
                     } else {
                         const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                        const cx<T> tq = Wt[q], tm = Wt[M - q];
-                        const cx<T> wq = Ww[q], wm = Ww[M - q];
+                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                        const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
                         const cx<T> U1 = cmul<T>(wq, rsplit<T>(zk, zm, tq));
                         const cx<T> U2 = cmul<T>(wm, rsplit<T>(zm, zk, tm));
                         const T Xq = (T)2 * U1.x * eig_factor<T>(S, L, KPHYS(q));
@@ -371,8 +373,8 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                     const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
                     hold[2 * it + 1] = rmerge<T>(Vh, Vh, th);
                 } else {
-                    const cx<T> wq = Ww[q], wm = Ww[M - q];
-                    const cx<T> tq = Wt[q], tm = Wt[M - q];
+                    const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
+                    const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
                     const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
                     const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
                     hold[2 * it] = rmerge<T>(Vk, Vm, tq);
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
                 } else {
                     const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
                     line_f[P(q)] = rmerge<T>(xk, xm, Wt[q]);
-                    line_f[P(M - q)] = rmerge<T>(xm, xk, Wt[M - q]);
+                    line_f[P(M - q)] = rmerge<T>(xm, xk, t_mirror<T>(Wt[q]));
                 }
             }
             __syncthreads();
@@ -407,6 +409,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     }
 
     // =============== INVERSE FFT + store (INV and MID)
+    if constexpr (OP == OP_FWD) return; else {
     fft_tile<true, T, LOGM>(line_f, jt, W);
     if (!Lio.valid) return;
     {
@@ -458,18 +461,23 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
             }
         }
     }
+    }
 }
 
 }  // namespace fpb
 
 #define FP_FFT_PICK(NAME, T, LO, HI)                                                   \
     namespace fpb {                                                                    \
-    template <int L> static FftKernelFn NAME##_one(bool s) {                           \
-        return s ? fft_pass_kernel<T, L, true> : fft_pass_kernel<T, L, false>;         \
+    template <int L, int OPV> static FftKernelFn NAME##_one(bool s) {                  \
+        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_kernel<T, L, false, OPV>; \
     }                                                                                  \
-    template <int L> static FftKernelFn NAME##_rec(int logM, bool s) {                 \
+    template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op) {         \
         if constexpr (L > HI) { return nullptr; }                                      \
-        else { return logM == L ? NAME##_one<L>(s) : NAME##_rec<L + 1>(logM, s); }     \
+        else {                                                                         \
+            if (logM != L) return NAME##_rec<L + 1>(logM, s, op);                      \
+            return op == OP_FWD ? NAME##_one<L, OP_FWD>(s)                             \
+                 : op == OP_INV ? NAME##_one<L, OP_INV>(s) : NAME##_one<L, OP_MID>(s); \
+        }                                                                              \
     }                                                                                  \
-    FftKernelFn NAME(int logM, bool s) { return NAME##_rec<LO>(logM, s); }             \
+    FftKernelFn NAME(int logM, bool s, int op) { return NAME##_rec<LO>(logM, s, op); } \
     }

@@ -32,10 +32,10 @@
 namespace fpb {
 
 using FftKernelFn = void (*)(const FftPass);
-FftKernelFn pick_fft_d_lo(int logM, bool strided);
-FftKernelFn pick_fft_d_hi(int logM, bool strided);
-FftKernelFn pick_fft_f_lo(int logM, bool strided);
-FftKernelFn pick_fft_f_hi(int logM, bool strided);
+FftKernelFn pick_fft_d_lo(int logM, bool strided, int op);
+FftKernelFn pick_fft_d_hi(int logM, bool strided, int op);
+FftKernelFn pick_fft_f_lo(int logM, bool strided, int op);
+FftKernelFn pick_fft_f_hi(int logM, bool strided, int op);
 
 // ----------------------------------------------------------------------------
 // dense engine: out_k = sum_j mat[k][j] * in_j, one tile of lines per CTA
@@ -198,9 +198,9 @@ size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes) {
 }
 
 template <typename T>
-static FftKernelFn pick_fft(int logM, bool strided) {
-    if (sizeof(T) == 8) return logM <= 8 ? pick_fft_d_lo(logM, strided) : pick_fft_d_hi(logM, strided);
-    return logM <= 8 ? pick_fft_f_lo(logM, strided) : pick_fft_f_hi(logM, strided);
+static FftKernelFn pick_fft(int logM, bool strided, int op) {
+    if (sizeof(T) == 8) return logM <= 8 ? pick_fft_d_lo(logM, strided, op) : pick_fft_d_hi(logM, strided, op);
+    return logM <= 8 ? pick_fft_f_lo(logM, strided, op) : pick_fft_f_hi(logM, strided, op);
 }
 
 static cudaError_t set_smem_attr() {
@@ -208,10 +208,11 @@ static cudaError_t set_smem_attr() {
     if (done) return cudaSuccess;
     cudaError_t e;
     for (int l = 4; l <= 12; ++l)
-        for (int s = 0; s < 2; ++s) {
-            if ((e = cudaFuncSetAttribute(pick_fft<double>(l, s), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-            if ((e = cudaFuncSetAttribute(pick_fft<float>(l, s), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-        }
+        for (int s = 0; s < 2; ++s)
+            for (int op = 0; op < 3; ++op) {
+                if ((e = cudaFuncSetAttribute(pick_fft<double>(l, s, op), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+                if ((e = cudaFuncSetAttribute(pick_fft<float>(l, s, op), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+            }
     if ((e = cudaFuncSetAttribute(dense_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(dense_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
     done = true;
@@ -224,7 +225,7 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     const int threads = p.lines << (p.logM - 4);
     const size_t smem = fft_pass_smem_bytes(p, f32 ? 4 : 8);
     const bool strided = p.family == FAM_STRIDED;
-    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided) : pick_fft<double>(p.logM, strided);
+    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op) : pick_fft<double>(p.logM, strided, p.op);
     if (!fn) return cudaErrorInvalidValue;
     fn<<<p.tiles, threads, smem, st>>>(p);
     return cudaGetLastError();

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -245,13 +246,23 @@ int fft_length(int bc, int kind, long long n, bool rfft) {
 
 const long long kDenseMax = 4096;
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    const int x = std::atoi(v);
+    return x > 0 ? x : dflt;
+}
+
 // choose the tile shape of an FFT pass
 void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long nb) {
     const int logTL = p.logM - 4;
     const int real_bytes = f32 ? 4 : 8;
     int lines;
+    // FP_TILE_THREADS_CONTIG / FP_TILE_BYTES_STRIDED: tuning overrides (benchmarks only)
+    static const int contig_threads = env_int("FP_TILE_THREADS_CONTIG", 128);
+    static const int strided_bytes = env_int("FP_TILE_BYTES_STRIDED", 128);
     if (p.family == FAM_CONTIG) {
-        lines = std::max(1, 256 >> logTL);
+        lines = std::max(1, contig_threads >> logTL);
         const long long nl = na * nb;
         while (lines > 1 && lines / 2 >= nl) lines /= 2;
         p.lines = lines;
@@ -264,7 +275,7 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
         p.nbt = 0;
     } else {
         const int eb = (in_cpx ? 2 : 1) * real_bytes;
-        lines = std::max(1, 128 / eb);
+        lines = std::max(1, strided_bytes / eb);
         while (lines > 1 && lines / 2 >= nb) lines /= 2;
         p.lines = lines;
         p.logLines = ilog2(lines);

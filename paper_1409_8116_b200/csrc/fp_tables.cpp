@@ -52,10 +52,30 @@ static void root(long long num, long long den, long double* re, long double* im)
     *im = -s;
 }
 
+// Per-stage Stockham twiddles, r-major (see stage_tw_offset in fp_common.cuh):
+// for every radix-16 stage with Ns = 2^l > 1, entries [r][e] = W_M^{r e M/(16 Ns)}.
+static void stage_twiddles(int M, std::vector<long double>& out) {
+    int logM = 0;
+    while ((1 << logM) < M) ++logM;
+    out.clear();
+    int l = (logM & 3) ? (logM & 3) : 4;
+    for (; l < logM; l += 4) {
+        const long long ns = 1LL << l;
+        const long long step = M >> (l + 4);
+        for (long long r = 0; r < 16; ++r)
+            for (long long e = 0; e < ns; ++e) {
+                long double re, im;
+                root((r * e * step) % M, M, &re, &im);
+                out.push_back(re);
+                out.push_back(im);
+            }
+    }
+    if (out.empty()) { out.push_back(1.0L); out.push_back(0.0L); }
+}
+
 void fft_tables(int n_real, int M, bool real_kind, std::vector<long double>& wfft,
                 std::vector<long double>& wt, std::vector<long double>& ww) {
-    wfft.assign(2 * (size_t)M, 0.0L);
-    for (int k = 0; k < M; ++k) root(k, M, &wfft[2 * k], &wfft[2 * k + 1]);
+    stage_twiddles(M, wfft);
     wt.clear();
     ww.clear();
     if (real_kind) {
