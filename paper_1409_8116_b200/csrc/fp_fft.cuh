@@ -1,6 +1,16 @@
-// fp_fft.cuh -- the FFT line-engine pass kernel (see fp_kernels.cu header for
-// the algorithm).  Instantiated per (precision, log2 FFT length, family) in the
-// fp_fft_*.cu translation units, which are compiled in parallel.
+// fp_fft.cuh -- the FFT line-engine pass kernels (see fp_kernels.cu header for
+// the algorithm).  Instantiated per (precision, log2 FFT length, family, op) in
+// the fp_fft_*.cu translation units, which are compiled in parallel.
+//
+// fft_pass_kernel: one tile of complete lines per CTA; every thread's global
+// loads are issued (into registers) before the first shared-memory store.
+// Operands are plan-typed (real T or complex T); strides are arbitrary.
+//
+// Thread mappings (nth = lines * M/16 threads, TL = M/16):
+//   line-major  (FFT stages, MID step):  line = tid / TL, jt = tid % TL
+//   I/O mapping (loads/stores):          CONTIG = line-major (lanes walk along a
+//     line), STRIDED = column-major (lanes walk across the W adjacent lines so
+//     each row segment of W elements is one coalesced access).
 #pragma once
 #include "fp_common.cuh"
 
@@ -8,348 +18,420 @@ namespace fpb {
 
 using FftKernelFn = void (*)(const FftPass);
 
-// the FFT pass kernel: compile-time FFT length M = 2^LOGM and line family.
-//
-// Thread mappings (nth = lines * M/16 threads, TL = M/16):
-//   line-major  (FFT stages, MID step):  line = tid / TL, jt = tid % TL
-//   I/O mapping (global loads/stores):   CONTIG = line-major (lanes walk along a
-//     line), STRIDED = column-major (lanes walk across the W adjacent lines so
-//     each row segment of W elements is one coalesced access).
-// Every per-thread loop has a compile-time trip count, and all of a thread's
-// global loads are issued before the first shared-memory store.
+template <int LOGM> struct Shape {
+    static constexpr int M = 1 << LOGM;
+    static constexpr int LOGTL = LOGM - 4;
+    static constexpr int TL = 1 << LOGTL;
+    static constexpr int HALF = M / 2;
+    static constexpr int LS = ((M + M / 16 + 1) & 1) ? (M + M / 16 + 1) : (M + M / 16 + 2);
+};
 
+// does this (op, kind) read complex lines?
+template <int OP>
+__device__ __forceinline__ bool complex_input(const FftPass& p) {
+    if (OP == OP_INV) return p.ikind == IK_ICFFT || p.ikind == IK_IRFFT;
+    return p.fkind == FK_CFFT;
+}
+
+// ----------------------------------------------------------------------------
+// per-line bookkeeping of tile `tile` (threads < lines)
+template <bool STRIDED, int OP>
+__device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo* linfo) {
+    const int tid = threadIdx.x;
+    const Geometry& g = p.g;
+    if (tid >= p.lines) return;
+    LineInfo L;
+    int ia, ib;
+    bool valid;
+    if (!STRIDED) {
+        const long long l = (long long)tile * p.lines + tid;
+        valid = l < (long long)g.na * g.nb;
+        ia = valid ? (int)(l / g.nb) : 0;
+        ib = valid ? (int)(l % g.nb) : 0;
+    } else {
+        ia = tile / p.nbt;
+        ib = (tile % p.nbt) * p.lines + tid;
+        valid = ib < g.nb;
+        if (!valid) ib = 0;
+    }
+    L.valid = valid;
+    L.in_off = (long long)ia * g.in_sa + (long long)ib * g.in_sb;
+    L.out_off = (long long)ia * g.out_sa + (long long)ib * g.out_sb;
+    L.null_line = (ia == 0 && ib == 0);
+    double before = 0.0, a1 = 0.0, a2 = 0.0;
+    int nafter = 0;
+    if (OP == OP_MID) {
+        const bool ha = p.s.lam_a != nullptr, hb = p.s.lam_b != nullptr;
+        const double la = ha ? p.s.lam_a[ia] : 0.0;
+        const double lb = hb ? p.s.lam_b[ib] : 0.0;
+        if (ha && p.s.pos_a < p.s.pos_t) before += la;
+        if (hb && p.s.pos_b < p.s.pos_t) before += lb;
+        if (ha && p.s.pos_a > p.s.pos_t) { a1 = la; nafter = 1; }
+        if (hb && p.s.pos_b > p.s.pos_t) { if (nafter == 0) a1 = lb; else a2 = lb; ++nafter; }
+    }
+    L.before = before; L.after1 = a1; L.after2 = a2; L.nafter = nafter; L.pad = 0;
+    linfo[tid] = L;
+}
+
+// ----------------------------------------------------------------------------
+// line loads (all of a thread's loads issued before any use; the uniform
+// valid / unit-stride conditions are hoisted out of the unrolled loops)
+template <typename T, int CNT, int STEP>
+__device__ __forceinline__ void load_cx(cx<T>* v, const cx<T>* base, long long st, bool valid, bool unit) {
+    if (!valid) {
+#pragma unroll
+        for (int it = 0; it < CNT; ++it) v[it] = mkc<T>(0, 0);
+    } else if (unit) {
+#pragma unroll
+        for (int it = 0; it < CNT; ++it) v[it] = __ldg(base + it * STEP);
+    } else {
+        const long long step = (long long)STEP * st;
+#pragma unroll
+        for (int it = 0; it < CNT; ++it, base += step) v[it] = __ldg(base);
+    }
+}
+template <typename T, int CNT, int STEP>
+__device__ __forceinline__ void load_real(T* v, const T* base, long long st, bool valid) {
+    if (!valid) {
+#pragma unroll
+        for (int it = 0; it < CNT; ++it) v[it] = 0;
+    } else {
+        const long long step = (long long)STEP * st;
+#pragma unroll
+        for (int it = 0; it < CNT; ++it, base += step) v[it] = __ldg(base);
+    }
+}
+// CONTIG real pairs (x_{2p}, x_{2p+1}), p = bio + TL it
+template <typename T, int TL>
+__device__ __forceinline__ void load_pairs(cx<T>* v, const T* line, long long st, bool valid, bool vec, int bio) {
+    if (!valid) {
+#pragma unroll
+        for (int it = 0; it < 16; ++it) v[it] = mkc<T>(0, 0);
+    } else if (vec) {
+        const cx<T>* s = reinterpret_cast<const cx<T>*>(line) + bio;
+#pragma unroll
+        for (int it = 0; it < 16; ++it) v[it] = __ldg(s + it * TL);
+    } else {
+        const T* s = line + (long long)(2 * bio) * st;
+        const long long step = (long long)(2 * TL) * st;
+#pragma unroll
+        for (int it = 0; it < 16; ++it, s += step) v[it] = mkc<T>(__ldg(s), __ldg(s + st));
+    }
+}
+
+// ----------------------------------------------------------------------------
+// placement: line values -> padded complex tile in the layout the FFT expects
+// (Makhoul reordering / half-length packing for real kinds).  Returns the
+// non-finite flag of the values it read.
 template <typename T, int LOGM, bool STRIDED, int OP>
-__global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int M = 1 << LOGM;
-    constexpr int LOGTL = LOGM - 4;
-    constexpr int TL = 1 << LOGTL;
-    constexpr int HALF = M / 2;
-    constexpr int LS = ((M + M / 16 + 1) & 1) ? (M + M / 16 + 1) : (M + M / 16 + 2);
-    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
-    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw + linfo_bytes(p.lines));
+__device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio, cx<T>* line_io, int bio) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, TL = S::TL;
+    constexpr bool fwd_in = OP != OP_INV;
+    constexpr int n = 2 * M;   // real kinds (unused by the complex ones)
+    T* zr_io = reinterpret_cast<T*>(line_io);
+    bool bad = false;
+    const bool chk = p.nonfinite != nullptr;
+    const T* rline = reinterpret_cast<const T*>(p.g.in) + Lio.in_off;
+    const cx<T>* cline = reinterpret_cast<const cx<T>*>(p.g.in) + Lio.in_off;
+    const long long st = p.g.in_st;
+    cx<T> v[16];
+    if (fwd_in && p.fkind != FK_CFFT) {
+        const int kind = p.fkind;
+        if (!STRIDED) {
+            load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const int pi = bio + it * TL;
+                T x0 = v[it].x, x1 = v[it].y;
+                if (chk) bad |= !(finite_t(x0) && finite_t(x1));
+                if (kind == FK_RFFT) {
+                    line_io[P(pi)] = mkc<T>(x0, x1);
+                } else {
+                    if (kind == FK_DST2) x1 = -x1;
+                    const int pa = pi, pb = n - 1 - pi;  // Makhoul: v_pi = x_j, v_{n-1-pi} = x_{j+1}
+                    zr_io[2 * P(pa >> 1) + (pa & 1)] = x0;
+                    zr_io[2 * P(pb >> 1) + (pb & 1)] = x1;
+                }
+            }
+        } else {
+            T xr[32];
+            load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
+#pragma unroll
+            for (int it = 0; it < 32; ++it) {
+                const int j = bio + it * TL;
+                T x = xr[it];
+                if (chk) bad |= !finite_t(x);
+                int pv;
+                if (kind == FK_RFFT) pv = j;
+                else {
+                    pv = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
+                    if (kind == FK_DST2 && (j & 1)) x = -x;
+                }
+                zr_io[2 * P(pv >> 1) + (pv & 1)] = x;
+            }
+        }
+    } else if (complex_input<OP>(p)) {
+        load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, !STRIDED && st == 1);
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+            line_io[P(bio + it * TL)] = v[it];
+        }
+    } else {
+        // DCT-III / DST-III: real spectrum of n = 2M entries
+        const bool dst = p.ikind == IK_DST3;
+        if (!STRIDED) {
+            load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const int k = 2 * (bio + it * TL);
+                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+                zr_io[PR(dst ? n - 1 - k : k)] = v[it].x;
+                zr_io[PR(dst ? n - 2 - k : k + 1)] = v[it].y;
+            }
+        } else {
+            T xr[32];
+            load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
+#pragma unroll
+            for (int it = 0; it < 32; ++it) {
+                const int k = bio + it * TL;
+                if (chk) bad |= !finite_t(xr[it]);
+                zr_io[PR(dst ? n - 1 - k : k)] = xr[it];
+            }
+        }
+    }
+    return bad && Lio.valid;
+}
 
+// the Nyquist entry k = M of an inverse half spectrum always comes from HBM
+template <typename T, int LOGM, int OP>
+__device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& Lio, cx<T>* line_io, int bio) {
+    constexpr int M = 1 << LOGM;
+    if (OP != OP_INV || p.ikind != IK_IRFFT || bio != 0) return false;
+    cx<T> xm = mkc<T>(0, 0);
+    if (Lio.valid) xm = __ldg(reinterpret_cast<const cx<T>*>(p.g.in) + Lio.in_off + (long long)M * p.g.in_st);
+    line_io[P(M)] = xm;
+    return Lio.valid && p.nonfinite && !(finite_t(xm.x) && finite_t(xm.y));
+}
+
+// ----------------------------------------------------------------------------
+// Quad / pair helpers.  In every quad loop q = j + TL*it; only it == 0 can give
+// q == 0 (the DC / Nyquist / self-paired special case), so that iteration is
+// peeled and the seven others run branch-free.
+
+// 2 V_k: the real-FFT untangle without its factor 1/2
+template <typename T>
+__device__ __forceinline__ cx<T> rsplit2(cx<T> zk, cx<T> zm, cx<T> tk) {
+    const cx<T> A = mkc<T>(zk.x + zm.x, zk.y - zm.y);
+    const cx<T> B = mkc<T>(zk.x - zm.x, zk.y + zm.y);
+    const cx<T> tB = cmul<T>(tk, B);
+    return mkc<T>(A.x + tB.y, A.y - tB.x);
+}
+
+// cst / lam for modes off the null mode (lam < 0 strictly): no select needed
+template <typename T>
+__device__ __forceinline__ T eig_factor_nz(const Scaling& s, const LineInfo& L, int kt, double cst) {
+    double lam = L.before + __ldg(&s.lam_t[kt]);
+    if (L.nafter > 0) lam += L.after1;
+    if (L.nafter > 1) lam += L.after2;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
+    double e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    return (T)(cst * r);
+}
+
+// ----------------------------------------------------------------------------
+// transform + post/mid/pre + store of one placed tile (contains barriers;
+// every thread of the CTA must call it).
+template <typename T, int LOGM, bool STRIDED, int OP>
+__device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, LS = S::LS;
+    constexpr bool fwd_in = OP != OP_INV;
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
-    const int n = p.n;
+    constexpr int n = 2 * M;   // real kinds (unused by the complex ones)
     const void* __restrict__ W = p.wfft;
     const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
     const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
     const Geometry& g = p.g;
-
-    // ---- per-line setup
-    if (tid < Lc) {
-        LineInfo L;
-        int ia, ib;
-        bool valid;
-        if (!STRIDED) {
-            const long long l = (long long)blockIdx.x * Lc + tid;
-            valid = l < (long long)g.na * g.nb;
-            ia = valid ? (int)(l / g.nb) : 0;
-            ib = valid ? (int)(l % g.nb) : 0;
-        } else {
-            ia = blockIdx.x / p.nbt;
-            ib = (blockIdx.x % p.nbt) * Lc + tid;
-            valid = ib < g.nb;
-            if (!valid) ib = 0;
-        }
-        L.valid = valid;
-        L.in_off = (long long)ia * g.in_sa + (long long)ib * g.in_sb;
-        L.out_off = (long long)ia * g.out_sa + (long long)ib * g.out_sb;
-        L.null_line = (ia == 0 && ib == 0);
-        double before = 0.0, a1 = 0.0, a2 = 0.0;
-        int nafter = 0;
-        if (OP == OP_MID) {
-            const bool ha = p.s.lam_a != nullptr, hb = p.s.lam_b != nullptr;
-            const double la = ha ? p.s.lam_a[ia] : 0.0;
-            const double lb = hb ? p.s.lam_b[ib] : 0.0;
-            if (ha && p.s.pos_a < p.s.pos_t) before += la;
-            if (hb && p.s.pos_b < p.s.pos_t) before += lb;
-            if (ha && p.s.pos_a > p.s.pos_t) { a1 = la; nafter = 1; }
-            if (hb && p.s.pos_b > p.s.pos_t) { if (nafter == 0) a1 = lb; else a2 = lb; ++nafter; }
-        }
-        L.before = before; L.after1 = a1; L.after2 = a2; L.nafter = nafter; L.pad = 0;
-        linfo[tid] = L;
-    }
-    __syncthreads();
-
-    const int lf = tid >> LOGTL;          // line-major mapping
+    const int lf = tid >> LOGTL;
     const int jt = tid & (TL - 1);
-    const int lio = STRIDED ? (tid & (Lc - 1)) : lf;   // I/O mapping
+    const int lio = STRIDED ? (tid & (Lc - 1)) : lf;
     const int bio = STRIDED ? (tid >> logL) : jt;
     cx<T>* line_f = sm + lf * LS;
     cx<T>* line_io = sm + lio * LS;
-    T* zr_io = reinterpret_cast<T*>(line_io);
+    const T* zr_io = reinterpret_cast<const T*>(line_io);
     const LineInfo Lio = linfo[lio];
-    constexpr bool fwd_in = OP != OP_INV;
-    bool bad = false;
 
-    // =============== LOAD (batched: 16 complex / 32 real values per thread in flight)
-    {
-        cx<T> v[16];
-        if (fwd_in && p.fkind != FK_CFFT) {
-            const int kind = p.fkind;
-            if (!STRIDED) {
-                // pairs (x_j, x_{j+1}), j = 2 (bio + TL it)
-                if (Lio.valid) {
-                    if (p.vec_in) {
-                        const cx<T>* src = reinterpret_cast<const cx<T>*>(reinterpret_cast<const T*>(g.in) + Lio.in_off) + bio;
-#pragma unroll
-                        for (int it = 0; it < 16; ++it) v[it] = src[it * TL];
-                    } else {
-#pragma unroll
-                        for (int it = 0; it < 16; ++it) {
-                            const long long off = Lio.in_off + (long long)(2 * (bio + it * TL)) * g.in_st;
-                            v[it] = mkc<T>(ld_real<T>(g.in, g.in_type, off), ld_real<T>(g.in, g.in_type, off + g.in_st));
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int it = 0; it < 16; ++it) v[it] = mkc<T>(0, 0);
-                }
-#pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const int pi = bio + it * TL;
-                    T x0 = v[it].x, x1 = v[it].y;
-                    if (p.nonfinite) bad |= !(finite_t(x0) && finite_t(x1));
-                    if (kind == FK_RFFT) {
-                        line_io[P(pi)] = mkc<T>(x0, x1);
-                    } else {
-                        if (kind == FK_DST2) x1 = -x1;
-                        const int pa = pi, pb = n - 1 - pi;  // Makhoul: v_pi = x_j, v_{n-1-pi} = x_{j+1}
-                        zr_io[2 * P(pa >> 1) + (pa & 1)] = x0;
-                        zr_io[2 * P(pb >> 1) + (pb & 1)] = x1;
-                    }
-                }
-            } else {
-                // rows j = bio + TL it, it < 32 (n = 2M rows)
-                T xr[32];
-                if (Lio.valid) {
-                    const long long st = g.in_st;
-                    const long long off0 = Lio.in_off + (long long)bio * st;
-#pragma unroll
-                    for (int it = 0; it < 32; ++it) xr[it] = ld_real<T>(g.in, g.in_type, off0 + (long long)(it * TL) * st);
-                } else {
-#pragma unroll
-                    for (int it = 0; it < 32; ++it) xr[it] = 0;
-                }
-#pragma unroll
-                for (int it = 0; it < 32; ++it) {
-                    const int j = bio + it * TL;
-                    T x = xr[it];
-                    if (p.nonfinite) bad |= !finite_t(x);
-                    int pv;
-                    if (kind == FK_RFFT) pv = j;
-                    else {
-                        pv = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-                        if (kind == FK_DST2 && (j & 1)) x = -x;
-                    }
-                    zr_io[2 * P(pv >> 1) + (pv & 1)] = x;
-                }
-            }
-        } else if (fwd_in || p.ikind == IK_ICFFT || p.ikind == IK_IRFFT) {
-            // complex lines in natural order (CFFT forward, ICFFT / IRFFT inverse)
-            if (Lio.valid) {
-                const long long st = g.in_st;
-                const long long off0 = Lio.in_off + (long long)bio * st;
-#pragma unroll
-                for (int it = 0; it < 16; ++it) v[it] = ld_cx<T>(g.in, g.in_type, off0 + (long long)(it * TL) * st);
-            } else {
-#pragma unroll
-                for (int it = 0; it < 16; ++it) v[it] = mkc<T>(0, 0);
-            }
-#pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                if (p.nonfinite) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-                line_io[P(bio + it * TL)] = v[it];
-            }
-            if (!fwd_in && p.ikind == IK_IRFFT && bio == 0) {
-                // the Nyquist entry k = M of the half spectrum
-                cx<T> xm = mkc<T>(0, 0);
-                if (Lio.valid) xm = ld_cx<T>(g.in, g.in_type, Lio.in_off + (long long)M * g.in_st);
-                if (p.nonfinite) bad |= !(finite_t(xm.x) && finite_t(xm.y));
-                line_io[P(M)] = xm;
-            }
-        } else {
-            // DCT-III / DST-III: real spectrum of n = 2M entries
-            const bool dst = p.ikind == IK_DST3;
-            if (!STRIDED && p.vec_in) {
-                if (Lio.valid) {
-                    const cx<T>* src = reinterpret_cast<const cx<T>*>(reinterpret_cast<const T*>(g.in) + Lio.in_off) + bio;
-#pragma unroll
-                    for (int it = 0; it < 16; ++it) v[it] = src[it * TL];
-                } else {
-#pragma unroll
-                    for (int it = 0; it < 16; ++it) v[it] = mkc<T>(0, 0);
-                }
-#pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const int k = 2 * (bio + it * TL);
-                    if (p.nonfinite) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-                    zr_io[PR(dst ? n - 1 - k : k)] = v[it].x;
-                    zr_io[PR(dst ? n - 2 - k : k + 1)] = v[it].y;
-                }
-            } else {
-                // generic: CONTIG rows k = 2(bio + TL it) + {0,1}; STRIDED rows k = bio + TL it
-                T xr[32];
-                const long long st = g.in_st;
-#pragma unroll
-                for (int it = 0; it < 32; ++it) {
-                    const int k = STRIDED ? (bio + it * TL) : (2 * (bio + (it >> 1) * TL) + (it & 1));
-                    xr[it] = Lio.valid ? ld_real<T>(g.in, g.in_type, Lio.in_off + (long long)k * st) : (T)0;
-                }
-#pragma unroll
-                for (int it = 0; it < 32; ++it) {
-                    const int k = STRIDED ? (bio + it * TL) : (2 * (bio + (it >> 1) * TL) + (it & 1));
-                    if (p.nonfinite) bad |= !finite_t(xr[it]);
-                    zr_io[PR(dst ? n - 1 - k : k)] = xr[it];
-                }
-            }
-        }
-    }
-    if (bad) *p.nonfinite = 1;
-    __syncthreads();
-
-    // =============== FORWARD FFT (+ post / mid)
     if constexpr (fwd_in) {
         fft_tile<false, T, LOGM>(line_f, jt, W);
 
         if constexpr (OP == OP_FWD) {
             const int kind = p.fkind;
             const T om = (T)p.out_mult;
-            if (!Lio.valid) return;
-            const long long ob = Lio.out_off;
-            const long long os = g.out_st;
-            if (kind == FK_CFFT) {
+            if (Lio.valid) {
+                const long long ob = Lio.out_off;
+                const long long os = g.out_st;
+                if (kind == FK_CFFT) {
+                    cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
+                    const long long step = (long long)TL * os;
 #pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const int k = bio + it * TL;
-                    st_cx<T>(g.out, g.out_type, ob + (long long)k * os, cscale<T>(line_io[P(k)], om));
-                }
-            } else if (kind == FK_RFFT) {
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int q = bio + it * TL;
-                    if (q == 0) {
-                        const cx<T> z0 = line_io[P(0)];
-                        st_cx<T>(g.out, g.out_type, ob, mkc<T>((z0.x + z0.y) * om, 0));
-                        st_cx<T>(g.out, g.out_type, ob + (long long)M * os, mkc<T>((z0.x - z0.y) * om, 0));
-                        const cx<T> zh = line_io[P(HALF)];
-                        st_cx<T>(g.out, g.out_type, ob + (long long)HALF * os, cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), om));
-                    } else {
+                    for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
+                } else if (kind == FK_RFFT) {
+                    cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + ob;
+                    cx<T>* pq = pb + (long long)bio * os;
+                    cx<T>* pm = pb + (long long)(M - bio) * os;
+                    const long long step = (long long)TL * os;
+                    const T omh = om * (T)0.5;
+                    auto pair = [&](int q) {
                         const cx<T> zk = line_io[P(q)], zm = line_io[P(M - q)];
                         const cx<T> tq = Wt[q];
-                        st_cx<T>(g.out, g.out_type, ob + (long long)q * os, cscale<T>(rsplit<T>(zk, zm, tq), om));
-                        st_cx<T>(g.out, g.out_type, ob + (long long)(M - q) * os, cscale<T>(rsplit<T>(zm, zk, t_mirror<T>(tq)), om));
-                    }
-                }
-            } else {
-                const bool dst = kind == FK_DST2;
-#define EMIT(K, X) st_real<T>(g.out, g.out_type, ob + (long long)(dst ? (n - 1 - (K)) : (K)) * os, (X) * om)
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int q = bio + it * TL;
-                    if (q == 0) {
+                        *pq = cscale<T>(rsplit2<T>(zk, zm, tq), omh);
+                        *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
+                    };
+                    if (bio == 0) {
                         const cx<T> z0 = line_io[P(0)];
-                        const cx<T> wM = Ww[M];
-                        EMIT(0, (T)2 * (z0.x + z0.y));
-                        EMIT(M, (T)2 * (z0.x - z0.y) * wM.x);
+                        pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
+                        pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
                         const cx<T> zh = line_io[P(HALF)];
-                        const cx<T> U = cmul<T>(Ww[HALF], rsplit<T>(zh, zh, Wt[HALF]));
-                        EMIT(HALF, (T)2 * U.x);
-                        EMIT(n - HALF, (T)-2 * U.y);
+                        pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
                     } else {
+                        pair(bio);
+                    }
+                    pq += step; pm -= step;
+#pragma unroll
+                    for (int it = 1; it < 8; ++it, pq += step, pm -= step) pair(bio + it * TL);
+                } else {
+                    // DCT-II quads {q, n-q, M-q, M+q} (DST-II: mirrored indices)
+                    const bool dst = kind == FK_DST2;
+                    T* const pb = reinterpret_cast<T*>(g.out) + ob;
+                    const long long s1 = dst ? -os : os;                      // direction of index k
+                    T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;   // address of k = 0
+                    T* pa = p0 + (long long)bio * s1;             // k = q
+                    T* pn = p0 + (long long)(n - bio) * s1;       // k = n - q
+                    T* pm = p0 + (long long)(M - bio) * s1;       // k = M - q
+                    T* pp = p0 + (long long)(M + bio) * s1;       // k = M + q
+                    const long long step = (long long)TL * s1;
+                    auto quad = [&](int q) {
                         const cx<T> zk = line_io[P(q)], zm = line_io[P(M - q)];
                         const cx<T> tq = Wt[q], wq = Ww[q];
-                        const cx<T> U1 = cmul<T>(wq, rsplit<T>(zk, zm, tq));
-                        const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit<T>(zm, zk, t_mirror<T>(tq)));
-                        EMIT(q, (T)2 * U1.x);
-                        EMIT(n - q, (T)-2 * U1.y);
-                        EMIT(M - q, (T)2 * U2.x);
-                        EMIT(M + q, (T)-2 * U2.y);
+                        const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));        // X_q = Re, X_{n-q} = -Im
+                        const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
+                        *pa = U1.x * om;
+                        *pn = -U1.y * om;
+                        *pm = U2.x * om;
+                        *pp = -U2.y * om;
+                    };
+                    if (bio == 0) {
+                        const cx<T> z0 = line_io[P(0)];
+                        const cx<T> wM = Ww[M];
+                        p0[0] = (T)2 * (z0.x + z0.y) * om;
+                        p0[(long long)M * s1] = (T)2 * (z0.x - z0.y) * wM.x * om;
+                        const cx<T> zh = line_io[P(HALF)];
+                        const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                        p0[(long long)HALF * s1] = U.x * om;
+                        p0[(long long)(n - HALF) * s1] = -U.y * om;
+                    } else {
+                        quad(bio);
                     }
+                    pa += step; pn -= step; pm -= step; pp += step;
+#pragma unroll
+                    for (int it = 1; it < 8; ++it, pa += step, pn -= step, pm -= step, pp += step) quad(bio + it * TL);
                 }
-#undef EMIT
             }
             return;
-        }
-
-        // ---- OP_MID: post -> capture -> scale -> pre, in place on each quad/pair
-        {
+        } else {
+            // ---- OP_MID: post -> capture -> scale -> pre, in place on each quad/pair
             const int kind = p.fkind;
-            const Scaling& S = p.s;
+            const Scaling& Sc = p.s;
             const LineInfo L = linfo[lf];
-            const bool cap = S.singular && S.dc_out && L.null_line && L.valid;
+            const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+            const double cst = Sc.bscale * Sc.inv_np;
             if (kind == FK_CFFT) {
+                if (jt == 0) {
+                    const cx<T> X = line_f[P(0)];
+                    if (cap) *Sc.dc_out = (double)X.x;
+                    line_f[P(0)] = cscale<T>(X, eig_factor<T>(Sc, L, 0));
+                } else {
+                    line_f[P(jt)] = cscale<T>(line_f[P(jt)], eig_factor_nz<T>(Sc, L, jt, cst));
+                }
 #pragma unroll
-                for (int it = 0; it < 16; ++it) {
+                for (int it = 1; it < 16; ++it) {
                     const int k = jt + it * TL;
-                    const cx<T> X = line_f[P(k)];
-                    if (cap && k == 0) *S.dc_out = (double)X.x;
-                    line_f[P(k)] = cscale<T>(X, eig_factor<T>(S, L, k));
+                    line_f[P(k)] = cscale<T>(line_f[P(k)], eig_factor_nz<T>(Sc, L, k, cst));
                 }
             } else if (kind == FK_RFFT) {
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int q = jt + it * TL;
-                    if (q == 0) {
-                        const cx<T> z0 = line_f[P(0)];
-                        T x0 = z0.x + z0.y, xM = z0.x - z0.y;
-                        if (cap) *S.dc_out = (double)x0;
-                        x0 *= eig_factor<T>(S, L, 0);
-                        xM *= eig_factor<T>(S, L, M);
-                        line_f[P(0)] = mkc<T>(x0 + xM, x0 - xM);
-                        const cx<T> zh = line_f[P(HALF)];
-                        const cx<T> xh = cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), eig_factor<T>(S, L, HALF));
-                        line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
-                    } else {
-                        const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                        const cx<T> xk = cscale<T>(rsplit<T>(zk, zm, tq), eig_factor<T>(S, L, q));
-                        const cx<T> xm = cscale<T>(rsplit<T>(zm, zk, tm), eig_factor<T>(S, L, M - q));
-                        line_f[P(q)] = rmerge<T>(xk, xm, tq);
-                        line_f[P(M - q)] = rmerge<T>(xm, xk, tm);
-                    }
+                const double csth = cst * 0.5;   // the untangle's 1/2
+                auto pair = [&](int q) {
+                    const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
+                    const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                    const cx<T> xk = cscale<T>(rsplit2<T>(zk, zm, tq), eig_factor_nz<T>(Sc, L, q, csth));
+                    const cx<T> xm = cscale<T>(rsplit2<T>(zm, zk, tm), eig_factor_nz<T>(Sc, L, M - q, csth));
+                    line_f[P(q)] = rmerge<T>(xk, xm, tq);
+                    line_f[P(M - q)] = rmerge<T>(xm, xk, tm);
+                };
+                if (jt == 0) {
+                    const cx<T> z0 = line_f[P(0)];
+                    T x0 = z0.x + z0.y, xM = z0.x - z0.y;
+                    if (cap) *Sc.dc_out = (double)x0;
+                    x0 *= eig_factor<T>(Sc, L, 0);
+                    xM *= eig_factor<T>(Sc, L, M);
+                    line_f[P(0)] = mkc<T>(x0 + xM, x0 - xM);
+                    const cx<T> zh = line_f[P(HALF)];
+                    const cx<T> xh = cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), eig_factor<T>(Sc, L, HALF));
+                    line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
+                } else {
+                    pair(jt);
                 }
+#pragma unroll
+                for (int it = 1; it < 8; ++it) pair(jt + it * TL);
             } else {
                 const bool dst = kind == FK_DST2;
 #define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
-#pragma unroll
-                for (int it = 0; it < 8; ++it) {
-                    const int q = jt + it * TL;
-                    if (q == 0) {
-                        const cx<T> z0 = line_f[P(0)];
-                        const cx<T> wM = Ww[M];
-                        T X0 = (T)2 * (z0.x + z0.y);
-                        T XM = (T)2 * (z0.x - z0.y) * wM.x;
-                        if (cap && !dst) *S.dc_out = (double)X0;
-                        X0 *= eig_factor<T>(S, L, KPHYS(0));
-                        XM *= eig_factor<T>(S, L, KPHYS(M));
-                        const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
-                        line_f[P(0)] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
-                        const cx<T> zh = line_f[P(HALF)];
-                        const cx<T> wh = Ww[HALF], th = Wt[HALF];
-                        const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
-                        const T Xa = (T)2 * U.x * eig_factor<T>(S, L, KPHYS(HALF));
-                        const T Xb = (T)-2 * U.y * eig_factor<T>(S, L, KPHYS(n - HALF));
-                        const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
-                        line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
-                    } else {
-                        const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                        const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                        const cx<T> U1 = cmul<T>(wq, rsplit<T>(zk, zm, tq));
-                        const cx<T> U2 = cmul<T>(wm, rsplit<T>(zm, zk, tm));
-                        const T Xq = (T)2 * U1.x * eig_factor<T>(S, L, KPHYS(q));
-                        const T Xnq = (T)-2 * U1.y * eig_factor<T>(S, L, KPHYS(n - q));
-                        const T Xmq = (T)2 * U2.x * eig_factor<T>(S, L, KPHYS(M - q));
-                        const T Xpq = (T)-2 * U2.y * eig_factor<T>(S, L, KPHYS(M + q));
-                        const cx<T> Vk = cmulc<T>(mkc<T>(Xq, -Xnq), wq);
-                        const cx<T> Vm = cmulc<T>(mkc<T>(Xmq, -Xpq), wm);
-                        line_f[P(q)] = rmerge<T>(Vk, Vm, tq);
-                        line_f[P(M - q)] = rmerge<T>(Vm, Vk, tm);
-                    }
+                // U = w * 2V gives X_k = Re U, X_{n-k} = -Im U (the 2 and the 1/2 cancel);
+                // the inverse takes V' = conj(w) (X_k f_k, -X_{n-k} f_{n-k}) = conj(w) (U.x f_k, U.y f_{n-k})
+                auto quad = [&](int q) {
+                    const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
+                    const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                    const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
+                    const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
+                    const cx<T> U2 = cmul<T>(wm, rsplit2<T>(zm, zk, tm));
+                    const cx<T> Y1 = mkc<T>(U1.x * eig_factor_nz<T>(Sc, L, KPHYS(q), cst),
+                                            U1.y * eig_factor_nz<T>(Sc, L, KPHYS(n - q), cst));
+                    const cx<T> Y2 = mkc<T>(U2.x * eig_factor_nz<T>(Sc, L, KPHYS(M - q), cst),
+                                            U2.y * eig_factor_nz<T>(Sc, L, KPHYS(M + q), cst));
+                    const cx<T> Vk = cmulc<T>(Y1, wq);
+                    const cx<T> Vm = cmulc<T>(Y2, wm);
+                    line_f[P(q)] = rmerge<T>(Vk, Vm, tq);
+                    line_f[P(M - q)] = rmerge<T>(Vm, Vk, tm);
+                };
+                if (jt == 0) {
+                    const cx<T> z0 = line_f[P(0)];
+                    const cx<T> wM = Ww[M];
+                    T X0 = (T)2 * (z0.x + z0.y);
+                    T XM = (T)2 * (z0.x - z0.y) * wM.x;
+                    if (cap && !dst) *Sc.dc_out = (double)X0;
+                    X0 *= eig_factor<T>(Sc, L, KPHYS(0));
+                    XM *= eig_factor<T>(Sc, L, KPHYS(M));
+                    const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                    line_f[P(0)] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                    const cx<T> zh = line_f[P(HALF)];
+                    const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                    const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
+                    const T Xa = (T)2 * U.x * eig_factor<T>(Sc, L, KPHYS(HALF));
+                    const T Xb = (T)-2 * U.y * eig_factor<T>(Sc, L, KPHYS(n - HALF));
+                    const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
+                    line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
+                } else {
+                    quad(jt);
                 }
+#pragma unroll 1
+                for (int it = 1; it < 8; ++it) quad(jt + it * TL);
 #undef KPHYS
             }
             __syncthreads();
@@ -361,123 +443,161 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
             // two-phase: the real-valued view overlaps the complex slots
             const T* zr = reinterpret_cast<const T*>(line_f);
             cx<T> hold[16];
-#pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const int q = jt + it * TL;
-                if (q == 0) {
-                    const T X0 = zr[PR(0)], XM = zr[PR(M)];
-                    const cx<T> wM = Ww[M];
-                    const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
-                    hold[2 * it] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
-                    const cx<T> wh = Ww[HALF], th = Wt[HALF];
-                    const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
-                    hold[2 * it + 1] = rmerge<T>(Vh, Vh, th);
-                } else {
-                    const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                    const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                    const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
-                    const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
-                    hold[2 * it] = rmerge<T>(Vk, Vm, tq);
-                    hold[2 * it + 1] = rmerge<T>(Vm, Vk, tm);
-                }
+            auto quad = [&](int q, int it) {
+                const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
+                const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
+                const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
+                hold[2 * it] = rmerge<T>(Vk, Vm, tq);
+                hold[2 * it + 1] = rmerge<T>(Vm, Vk, tm);
+            };
+            if (jt == 0) {
+                const T X0 = zr[PR(0)], XM = zr[PR(M)];
+                const cx<T> wM = Ww[M];
+                const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                hold[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
+                hold[1] = rmerge<T>(Vh, Vh, th);
+            } else {
+                quad(jt, 0);
             }
-            __syncthreads();
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
+            for (int it = 1; it < 8; ++it) quad(jt + it * TL, it);
+            __syncthreads();
+            line_f[P(jt)] = hold[0];
+            line_f[P(jt == 0 ? HALF : M - jt)] = hold[1];
+#pragma unroll
+            for (int it = 1; it < 8; ++it) {
                 const int q = jt + it * TL;
                 line_f[P(q)] = hold[2 * it];
-                line_f[P(q == 0 ? HALF : M - q)] = hold[2 * it + 1];
+                line_f[P(M - q)] = hold[2 * it + 1];
             }
             __syncthreads();
         } else if (ik == IK_IRFFT) {
-#pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const int q = jt + it * TL;
-                if (q == 0) {
-                    const cx<T> x0 = line_f[P(0)], xM = line_f[P(M)];
-                    line_f[P(0)] = rmerge<T>(x0, xM, mkc<T>(1, 0));
-                    const cx<T> xh = line_f[P(HALF)];
-                    line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
-                } else {
-                    const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
-                    line_f[P(q)] = rmerge<T>(xk, xm, Wt[q]);
-                    line_f[P(M - q)] = rmerge<T>(xm, xk, t_mirror<T>(Wt[q]));
-                }
+            auto pair = [&](int q) {
+                const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
+                const cx<T> tq = Wt[q];
+                line_f[P(q)] = rmerge<T>(xk, xm, tq);
+                line_f[P(M - q)] = rmerge<T>(xm, xk, t_mirror<T>(tq));
+            };
+            if (jt == 0) {
+                const cx<T> x0 = line_f[P(0)], xM = line_f[P(M)];
+                line_f[P(0)] = rmerge<T>(x0, xM, mkc<T>(1, 0));
+                const cx<T> xh = line_f[P(HALF)];
+                line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
+            } else {
+                pair(jt);
             }
+#pragma unroll
+            for (int it = 1; it < 8; ++it) pair(jt + it * TL);
             __syncthreads();
         }
     }
 
-    // =============== INVERSE FFT + store (INV and MID)
-    if constexpr (OP == OP_FWD) return; else {
-    fft_tile<true, T, LOGM>(line_f, jt, W);
-    if (!Lio.valid) return;
-    {
+    if constexpr (OP != OP_FWD) {
+        // =============== INVERSE FFT + store (INV and MID)
+        fft_tile<true, T, LOGM>(line_f, jt, W);
+        if (!Lio.valid) return;
         const int ik = p.ikind;
         const T om = (T)p.out_mult;
         const long long ob = Lio.out_off;
         const long long os = g.out_st;
         if (ik == IK_ICFFT) {
+            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
+            const long long step = (long long)TL * os;
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const int k = bio + it * TL;
-                st_cx<T>(g.out, g.out_type, ob + (long long)k * os, cscale<T>(line_io[P(k)], om));
-            }
+            for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
         } else {
             const bool dct = ik != IK_IRFFT;
             const bool dst = ik == IK_DST3;
+            T* const pb = reinterpret_cast<T*>(g.out) + ob;
             if (!STRIDED) {
+                // output pairs (x_{2m}, x_{2m+1}), m = bio + TL it
+                T xv[32];
 #pragma unroll
                 for (int it = 0; it < 16; ++it) {
-                    const int m = bio + it * TL;   // output pair (x_{2m}, x_{2m+1})
+                    const int m = bio + it * TL;
                     T x0, x1;
                     if (dct) {
-                        const int pa = m, pb = n - 1 - m;
+                        const int pa = m, pbv = n - 1 - m;
                         x0 = zr_io[2 * P(pa >> 1) + (pa & 1)];
-                        x1 = zr_io[2 * P(pb >> 1) + (pb & 1)];
+                        x1 = zr_io[2 * P(pbv >> 1) + (pbv & 1)];
                         if (dst) x1 = -x1;
                     } else {
                         const cx<T> v = line_io[P(m)];
                         x0 = v.x; x1 = v.y;
                     }
-                    x0 *= om; x1 *= om;
-                    const long long off = ob + (long long)(2 * m) * os;
-                    if (p.vec_out) {
-                        *reinterpret_cast<cx<T>*>(reinterpret_cast<T*>(g.out) + off) = mkc<T>(x0, x1);
-                    } else {
-                        st_real<T>(g.out, g.out_type, off, x0);
-                        st_real<T>(g.out, g.out_type, off + os, x1);
-                    }
+                    xv[2 * it] = x0 * om;
+                    xv[2 * it + 1] = x1 * om;
+                }
+                if (p.vec_out) {
+                    cx<T>* po = reinterpret_cast<cx<T>*>(pb) + bio;
+#pragma unroll
+                    for (int it = 0; it < 16; ++it) po[it * TL] = mkc<T>(xv[2 * it], xv[2 * it + 1]);
+                } else {
+                    T* po = pb + (long long)(2 * bio) * os;
+                    const long long step = (long long)(2 * TL) * os;
+#pragma unroll
+                    for (int it = 0; it < 16; ++it, po += step) { po[0] = xv[2 * it]; po[os] = xv[2 * it + 1]; }
                 }
             } else {
+                T* po = pb + (long long)bio * os;
+                const long long step = (long long)TL * os;
 #pragma unroll
-                for (int it = 0; it < 32; ++it) {
+                for (int it = 0; it < 32; ++it, po += step) {
                     const int j = bio + it * TL;
                     const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
                     T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
                     if (dst && (j & 1)) x = -x;
-                    st_real<T>(g.out, g.out_type, ob + (long long)j * os, x * om);
+                    *po = x * om;
                 }
             }
         }
     }
-    }
+}
+
+// ----------------------------------------------------------------------------
+// general path: one tile per CTA, loads straight from HBM
+template <typename T, int LOGM, bool STRIDED, int OP>
+__global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using S = Shape<LOGM>;
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw + linfo_bytes(p.lines));
+    setup_lines<STRIDED, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const int lio = STRIDED ? (tid & (p.lines - 1)) : (tid >> S::LOGTL);
+    const int bio = STRIDED ? (tid >> p.logLines) : (tid & (S::TL - 1));
+    const LineInfo Lio = linfo[lio];
+    cx<T>* line_io = sm + lio * S::LS;
+    bool bad = place_tile<T, LOGM, STRIDED, OP>(p, Lio, line_io, bio);
+    bad |= place_nyquist<T, LOGM, OP>(p, Lio, line_io, bio);
+    if (bad) *p.nonfinite = 1;
+    __syncthreads();
+    compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);
 }
 
 }  // namespace fpb
 
-#define FP_FFT_PICK(NAME, T, LO, HI)                                                   \
-    namespace fpb {                                                                    \
-    template <int L, int OPV> static FftKernelFn NAME##_one(bool s) {                  \
-        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_kernel<T, L, false, OPV>; \
-    }                                                                                  \
-    template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op) {         \
-        if constexpr (L > HI) { return nullptr; }                                      \
-        else {                                                                         \
-            if (logM != L) return NAME##_rec<L + 1>(logM, s, op);                      \
-            return op == OP_FWD ? NAME##_one<L, OP_FWD>(s)                             \
-                 : op == OP_INV ? NAME##_one<L, OP_INV>(s) : NAME##_one<L, OP_MID>(s); \
-        }                                                                              \
-    }                                                                                  \
-    FftKernelFn NAME(int logM, bool s, int op) { return NAME##_rec<LO>(logM, s, op); } \
+// (a persistent, TMA/cp.async double-buffered variant was measured slower on
+// B200 -- its staging tiles cut residency to 1-2 CTAs/SM -- and was removed)
+#define FP_FFT_PIPE_FN(T, L, s, OPV) ((FftKernelFn) nullptr)
+
+#define FP_FFT_PICK(NAME, T, LO, HI)                                                                  \
+    namespace fpb {                                                                                   \
+    template <int L, int OPV> static FftKernelFn NAME##_one(bool s, bool pipe) {                      \
+        if (pipe) return FP_FFT_PIPE_FN(T, L, s, OPV);                                                \
+        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_kernel<T, L, false, OPV>;              \
+    }                                                                                                 \
+    template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op, bool pipe) {             \
+        if constexpr (L > HI) { return nullptr; }                                                     \
+        else {                                                                                        \
+            if (logM != L) return NAME##_rec<L + 1>(logM, s, op, pipe);                               \
+            return op == OP_FWD ? NAME##_one<L, OP_FWD>(s, pipe)                                      \
+                 : op == OP_INV ? NAME##_one<L, OP_INV>(s, pipe) : NAME##_one<L, OP_MID>(s, pipe);    \
+        }                                                                                             \
+    }                                                                                                 \
+    FftKernelFn NAME(int logM, bool s, int op, bool pipe) { return NAME##_rec<LO>(logM, s, op, pipe); } \
     }

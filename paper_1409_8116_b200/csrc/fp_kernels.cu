@@ -27,15 +27,17 @@
 // Dense engine: direct summation with a host-built, correctly rounded matrix
 //   for every other (kind, n) the reference supports (DST-I, DCT-I, odd n,
 //   tiny n).  Tile-exclusive, so in-place safe.
+#include <cstdlib>
+
 #include "fp_common.cuh"
 
 namespace fpb {
 
 using FftKernelFn = void (*)(const FftPass);
-FftKernelFn pick_fft_d_lo(int logM, bool strided, int op);
-FftKernelFn pick_fft_d_hi(int logM, bool strided, int op);
-FftKernelFn pick_fft_f_lo(int logM, bool strided, int op);
-FftKernelFn pick_fft_f_hi(int logM, bool strided, int op);
+FftKernelFn pick_fft_d_lo(int logM, bool strided, int op, bool pipe);
+FftKernelFn pick_fft_d_hi(int logM, bool strided, int op, bool pipe);
+FftKernelFn pick_fft_f_lo(int logM, bool strided, int op, bool pipe);
+FftKernelFn pick_fft_f_hi(int logM, bool strided, int op, bool pipe);
 
 // ----------------------------------------------------------------------------
 // dense engine: out_k = sum_j mat[k][j] * in_j, one tile of lines per CTA
@@ -192,15 +194,45 @@ __global__ void __launch_bounds__(256) mean_sub_kernel(const MeanPass p, int npa
 }
 
 // ----------------------------------------------------------------------------
+// dtype cast of a strided rhs into a dense plan-typed array (solver.py:213's
+// np.array(rhs, dtype=work_dtype)); only when the caller's rhs dtype differs
+// from the plan precision -- the FFT passes then read plan-typed operands only.
+template <typename Ti, typename To>
+__global__ void __launch_bounds__(256) cast_kernel(const Ti* __restrict__ in, CastPass p, To* __restrict__ out) {
+    const long long total = (long long)p.ext[0] * p.ext[1] * p.ext[2];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long k2 = i % p.ext[2];
+        const long long r = i / p.ext[2];
+        const long long k1 = r % p.ext[1];
+        const long long k0 = r / p.ext[1];
+        out[i] = (To)__ldg(in + k0 * p.st[0] + k1 * p.st[1] + k2 * p.st[2]);
+    }
+}
+
+cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* out, int out_type, cudaStream_t st) {
+    const long long total = (long long)p.ext[0] * p.ext[1] * p.ext[2];
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks < 1) blocks = 1;
+    if (in_type == ET_F32 && out_type == ET_F64)
+        cast_kernel<float, double><<<(int)blocks, 256, 0, st>>>((const float*)in, p, (double*)out);
+    else if (in_type == ET_F64 && out_type == ET_F32)
+        cast_kernel<double, float><<<(int)blocks, 256, 0, st>>>((const double*)in, p, (float*)out);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
 // launchers (host)
 size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes) {
     return linfo_bytes(p.lines) + (size_t)p.lines * p.ls * 2 * real_bytes;
 }
 
 template <typename T>
-static FftKernelFn pick_fft(int logM, bool strided, int op) {
-    if (sizeof(T) == 8) return logM <= 8 ? pick_fft_d_lo(logM, strided, op) : pick_fft_d_hi(logM, strided, op);
-    return logM <= 8 ? pick_fft_f_lo(logM, strided, op) : pick_fft_f_hi(logM, strided, op);
+static FftKernelFn pick_fft(int logM, bool strided, int op, bool pipe) {
+    if (sizeof(T) == 8) return logM <= 8 ? pick_fft_d_lo(logM, strided, op, pipe) : pick_fft_d_hi(logM, strided, op, pipe);
+    return logM <= 8 ? pick_fft_f_lo(logM, strided, op, pipe) : pick_fft_f_hi(logM, strided, op, pipe);
 }
 
 static cudaError_t set_smem_attr() {
@@ -209,10 +241,12 @@ static cudaError_t set_smem_attr() {
     cudaError_t e;
     for (int l = 4; l <= 12; ++l)
         for (int s = 0; s < 2; ++s)
-            for (int op = 0; op < 3; ++op) {
-                if ((e = cudaFuncSetAttribute(pick_fft<double>(l, s, op), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-                if ((e = cudaFuncSetAttribute(pick_fft<float>(l, s, op), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-            }
+            for (int op = 0; op < 3; ++op)
+                for (int pp = 0; pp < 2; ++pp) {
+                    FftKernelFn fd = pick_fft<double>(l, s, op, pp), ff = pick_fft<float>(l, s, op, pp);
+                    if (fd && (e = cudaFuncSetAttribute(fd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+                    if (ff && (e = cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+                }
     if ((e = cudaFuncSetAttribute(dense_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
     if ((e = cudaFuncSetAttribute(dense_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
     done = true;
@@ -223,9 +257,9 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     cudaError_t e = set_smem_attr();
     if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);
-    const size_t smem = fft_pass_smem_bytes(p, f32 ? 4 : 8);
     const bool strided = p.family == FAM_STRIDED;
-    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op) : pick_fft<double>(p.logM, strided, p.op);
+    const size_t smem = fft_pass_smem_bytes(p, f32 ? 4 : 8);
+    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false) : pick_fft<double>(p.logM, strided, p.op, false);
     if (!fn) return cudaErrorInvalidValue;
     fn<<<p.tiles, threads, smem, st>>>(p);
     return cudaGetLastError();

@@ -29,6 +29,7 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st);
 cudaError_t launch_dense_pass(const DensePass& p, bool f32, cudaStream_t st);
 cudaError_t launch_scale_pass(const ScalePass& p, bool f32, cudaStream_t st);
 cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st);
+cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* out, int out_type, cudaStream_t st);
 size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
 }  // namespace fpb
 
@@ -602,7 +603,8 @@ static size_t mean_bytes(const fp_plan* P) {
 FP_API fp_status fp_plan_workspace_bytes(const fp_plan* P, int out_dense, size_t* bytes) {
     if (!P || !bytes) return fail(FP_ERR_VALUE, "NULL argument");
     size_t b = cw_bytes(P);
-    if (P->need_rs && !out_dense) b += rs_bytes(P);
+    // with a strided `out` the real scratch (also the dtype-cast target) lives here
+    if (!out_dense) b += rs_bytes(P);
     b += mean_bytes(P);
     *bytes = b;
     return FP_OK;
@@ -655,6 +657,19 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
 
     void* cw = workspace;
     void* rsb = out_dense ? out : (void*)((char*)workspace + cw_bytes(P));
+    // rhs in another precision: cast once into the real scratch (dense, plan-typed)
+    const int plan_fp = P->f32 ? FP_F32 : FP_F64;
+    if (rhs_dtype != plan_fp) {
+        CastPass cp{};
+        for (int k = 0; k < 3; ++k) { cp.ext[k] = 1; cp.st[k] = 0; }
+        for (int a = 0; a < d; ++a) { cp.ext[3 - d + a] = (int)P->n[a]; cp.st[3 - d + a] = rs_s[a]; }
+        cudaError_t e = launch_cast(rhs, rhs_dtype == FP_F32 ? ET_F32 : ET_F64, cp, rsb, P->f32 ? ET_F32 : ET_F64,
+                                    (cudaStream_t)stream);
+        if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("cast launch failed: ") + cudaGetErrorString(e));
+        rhs = rsb;
+        rhs_dtype = plan_fp;
+        for (int a = 0; a < 3; ++a) rs_s[a] = (a < d) ? (out_dense ? os_s[a] : dense_r[a]) : 0;
+    }
     double* mean_ws = P->mean_fix ? (double*)((char*)workspace + need - mean_bytes(P)) : nullptr;
     const int plan_type = P->f32 ? ET_F32 : ET_F64;
     const int plan_ctype = P->f32 ? ET_C64 : ET_C128;
@@ -917,6 +932,11 @@ FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int
     const bool out_c = out_dtype == FP_C128 || out_dtype == FP_C64;
     if (cpx_kind != out_c) return fail(FP_ERR_VALUE, "output dtype does not match the transform kind");
     if (!cpx_kind && (in_dtype == FP_C128 || in_dtype == FP_C64)) return fail(FP_ERR_VALUE, "real transform of complex data");
+    {   // operands must be in the transform precision (complex kinds: complex input)
+        const int want_in = cpx_kind ? (T->f32 ? FP_C64 : FP_C128) : (T->f32 ? FP_F32 : FP_F64);
+        if (in_dtype != want_in || out_dtype != want_in)
+            return fail(FP_ERR_VALUE, "operand dtypes must match the transform precision (complex kinds take complex input)");
+    }
     DeviceGuard dg(T->device);
     int o[2] = {-1, -1}, k = 0;
     for (int a = 0; a < ndim; ++a) if (a != axis) o[k++] = a;

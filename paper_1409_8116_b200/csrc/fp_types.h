@@ -108,4 +108,9 @@ struct MeanPass {               // subtract the arithmetic mean (DCT-I plans)
 };
 constexpr int kMeanParts = 1184;  // 8 x 148 SMs
 
+struct CastPass {               // strided rhs -> dense plan-typed copy
+    int ext[3];
+    long long st[3];
+};
+
 }  // namespace fpb

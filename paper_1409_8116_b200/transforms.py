@@ -194,6 +194,8 @@ class TransformPlan:
         single = x.dtype in (t.float32, t.complex64)
         precision = nat.FP_F32 if single else nat.FP_F64
         out_dtype = (t.complex64 if single else t.complex128) if self.kind.is_complex else x.dtype
+        if self.kind.is_complex and not x.is_complex():
+            x = x.to(out_dtype)   # the ABI takes complex operands for DFT/IDFT
         nd = x.ndim
         ax = self.axis % nd
         # collapse to (pre, n, post) so any rank maps onto the 3D ABI
