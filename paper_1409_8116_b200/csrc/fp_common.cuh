@@ -120,8 +120,12 @@ __host__ __device__ constexpr int stage_tw_offset(int logM, int logNs) {
 }
 __host__ __device__ constexpr int stage_tw_total(int logM) { return stage_tw_offset(logM, logM); }
 
-template <int R, int LOGNS, bool INV, typename T, int LOGM>
-__device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* __restrict__ W) {
+template <int R, int LOGNS, bool INV, typename T, int LOGM, bool FROM_REG = false, bool TO_REG = false>
+__device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* __restrict__ W,
+                                               cx<T>* vio = nullptr) {
+    // FROM_REG: butterfly inputs come from vio[s] = z[jt + TL s] (the layout the
+    //           last radix-16 stage leaves in registers) instead of shared memory
+    // TO_REG:   outputs stay in registers: vio[r] = z[jt + TL r] (last stage only)
     constexpr int M = 1 << LOGM;
     constexpr int LOGR = LogR<R>::v;
     constexpr int NB = 16 / R;
@@ -133,7 +137,10 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* 
     for (int b = 0; b < NB; ++b) {
         const int j = jt + b * TL;
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[b * R + r] = line[P(j + r * STRIDE_IN)];
+        for (int r = 0; r < R; ++r) {
+            if constexpr (FROM_REG) v[b * R + r] = vio[b + NB * r];
+            else v[b * R + r] = line[P(j + r * STRIDE_IN)];
+        }
         if (LOGNS > 0) {
             const cx<T>* tw = reinterpret_cast<const cx<T>*>(W) + stage_tw_offset(LOGM, LOGNS) + (j & (NS - 1));
 #pragma unroll
@@ -143,6 +150,12 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* 
             }
         }
         dft_reg<R, INV, T>(v + b * R);
+    }
+    if constexpr (TO_REG) {
+        static_assert(NB == 1 && NS == TL, "only the last radix-16 stage keeps its outputs in registers");
+#pragma unroll
+        for (int r = 0; r < 16; ++r) vio[r] = v[r];
+        return;
     }
     __syncthreads();
 #pragma unroll
@@ -170,6 +183,37 @@ __device__ __forceinline__ void fft_tile(cx<T>* line, int jt, const void* __rest
     if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
     radix16_stages<REM, INV, T, LOGM>(line, jt, W);
+}
+
+template <int LOGNS, int LIMIT, bool INV, typename T, int LOGM>
+__device__ __forceinline__ void radix16_stages_upto(cx<T>* line, int jt, const void* __restrict__ W) {
+    if constexpr (LOGNS < LIMIT) {
+        stockham_stage<16, LOGNS, INV, T, LOGM>(line, jt, W);
+        radix16_stages_upto<LOGNS + 4, LIMIT, INV, T, LOGM>(line, jt, W);
+    }
+}
+
+// all stages; the last (radix-16, Ns = TL) keeps its outputs in registers:
+// v[r] = Z[jt + TL r]
+template <bool INV, typename T, int LOGM>
+__device__ __forceinline__ void fft_tile_to_reg(cx<T>* line, int jt, const void* __restrict__ W, cx<T>* v) {
+    constexpr int REM = LOGM & 3;
+    if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM>(line, jt, W);
+    if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
+    if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
+    constexpr int FIRST16 = REM;
+    if constexpr (LOGM - 4 > FIRST16) radix16_stages_upto<FIRST16, LOGM - 4, INV, T, LOGM>(line, jt, W);
+    stockham_stage<16, LOGM - 4, INV, T, LOGM, false, true>(line, jt, W, v);
+}
+
+// all stages; the first takes its inputs from registers v[s] = z[jt + TL s]
+template <bool INV, typename T, int LOGM>
+__device__ __forceinline__ void fft_tile_from_reg(cx<T>* line, int jt, const void* __restrict__ W, cx<T>* v) {
+    constexpr int REM = LOGM & 3;
+    if constexpr (REM == 1) { stockham_stage<2, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<1, INV, T, LOGM>(line, jt, W); }
+    if constexpr (REM == 2) { stockham_stage<4, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<2, INV, T, LOGM>(line, jt, W); }
+    if constexpr (REM == 3) { stockham_stage<8, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<3, INV, T, LOGM>(line, jt, W); }
+    if constexpr (REM == 0) { stockham_stage<16, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<4, INV, T, LOGM>(line, jt, W); }
 }
 
 // twiddles of the mirrored index M-q from those of q (n = 2M):

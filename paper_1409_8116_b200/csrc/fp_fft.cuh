@@ -215,6 +215,78 @@ __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& 
     return Lio.valid && p.nonfinite && !(finite_t(xm.x) && finite_t(xm.y));
 }
 
+// store of an inverse-transformed tile (natural-order data in shared memory)
+template <typename T, int LOGM, bool STRIDED>
+__device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, LS = S::LS;
+    constexpr int n = 2 * M;
+    const int tid = threadIdx.x;
+    const int Lc = p.lines, logL = p.logLines;
+    const Geometry& g = p.g;
+    const int lio = STRIDED ? (tid & (Lc - 1)) : (tid >> LOGTL);
+    const int bio = STRIDED ? (tid >> logL) : (tid & (TL - 1));
+    cx<T>* line_io = sm + lio * LS;
+    const T* zr_io = reinterpret_cast<const T*>(line_io);
+    const LineInfo Lio = linfo[lio];
+        if (!Lio.valid) return;
+        const int ik = p.ikind;
+        const T om = (T)p.out_mult;
+        const long long ob = Lio.out_off;
+        const long long os = g.out_st;
+        if (ik == IK_ICFFT) {
+            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
+            const long long step = (long long)TL * os;
+#pragma unroll
+            for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
+        } else {
+            const bool dct = ik != IK_IRFFT;
+            const bool dst = ik == IK_DST3;
+            T* const pb = reinterpret_cast<T*>(g.out) + ob;
+            if (!STRIDED) {
+                // output pairs (x_{2m}, x_{2m+1}), m = bio + TL it
+                T xv[32];
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int m = bio + it * TL;
+                    T x0, x1;
+                    if (dct) {
+                        const int pa = m, pbv = n - 1 - m;
+                        x0 = zr_io[2 * P(pa >> 1) + (pa & 1)];
+                        x1 = zr_io[2 * P(pbv >> 1) + (pbv & 1)];
+                        if (dst) x1 = -x1;
+                    } else {
+                        const cx<T> v = line_io[P(m)];
+                        x0 = v.x; x1 = v.y;
+                    }
+                    xv[2 * it] = x0 * om;
+                    xv[2 * it + 1] = x1 * om;
+                }
+                if (p.vec_out) {
+                    cx<T>* po = reinterpret_cast<cx<T>*>(pb) + bio;
+#pragma unroll
+                    for (int it = 0; it < 16; ++it) po[it * TL] = mkc<T>(xv[2 * it], xv[2 * it + 1]);
+                } else {
+                    T* po = pb + (long long)(2 * bio) * os;
+                    const long long step = (long long)(2 * TL) * os;
+#pragma unroll
+                    for (int it = 0; it < 16; ++it, po += step) { po[0] = xv[2 * it]; po[os] = xv[2 * it + 1]; }
+                }
+            } else {
+                T* po = pb + (long long)bio * os;
+                const long long step = (long long)TL * os;
+#pragma unroll
+                for (int it = 0; it < 32; ++it, po += step) {
+                    const int j = bio + it * TL;
+                    const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
+                    T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
+                    if (dst && (j & 1)) x = -x;
+                    *po = x * om;
+                }
+            }
+        }
+    }
+
 // ----------------------------------------------------------------------------
 // Quad / pair helpers.  In every quad loop q = j + TL*it; only it == 0 can give
 // q == 0 (the DC / Nyquist / self-paired special case), so that iteration is
@@ -498,62 +570,258 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     if constexpr (OP != OP_FWD) {
         // =============== INVERSE FFT + store (INV and MID)
         fft_tile<true, T, LOGM>(line_f, jt, W);
-        if (!Lio.valid) return;
-        const int ik = p.ikind;
+        compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Register path (M <= 512, i.e. TL <= 32 threads per line).  After the last
+// radix-16 stage thread jt holds Z[jt + TL r] in registers; the partner of
+// index k = jt + TL r is M - k = (TL - jt) + TL (15 - r), held by lane TL - jt
+// of the same warp.  Post-processing, the MID scale and the inverse
+// pre-processing then exchange the mirrored halves with warp shuffles instead
+// of a shared-memory round trip, and the inverse FFT starts from registers.
+template <typename T>
+__device__ __forceinline__ cx<T> shfl_cx(cx<T> v, int src) {
+    return mkc<T>(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// pz[r] = Z[M - (jt + TL r)] for r < 8 (jt = 0 uses its own registers)
+template <typename T>
+__device__ __forceinline__ void fetch_mirror(const cx<T>* v, cx<T>* pz, int jt, int partner) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) pz[r] = shfl_cx<T>(v[15 - r], partner);
+    if (jt == 0) {
+#pragma unroll
+        for (int r = 1; r < 8; ++r) pz[r] = v[16 - r];
+    }
+}
+// inverse of fetch_mirror: v[s], s >= 8, from the partner's pz (jt = 0: own)
+// (v[8] of jt = 0 must be supplied by the caller: the self-paired HALF entry)
+template <typename T>
+__device__ __forceinline__ void return_mirror(cx<T>* v, const cx<T>* pz, int jt, int partner, cx<T> half0) {
+#pragma unroll
+    for (int s = 8; s < 16; ++s) v[s] = shfl_cx<T>(pz[15 - s], partner);
+    if (jt == 0) {
+        v[8] = half0;
+#pragma unroll
+        for (int s = 9; s < 16; ++s) v[s] = pz[16 - s];
+    }
+}
+
+template <typename T, int LOGM, bool STRIDED, int OP>
+__device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, LS = S::LS;
+    constexpr int n = 2 * M;
+    const int tid = threadIdx.x;
+    const int Lc = p.lines, logL = p.logLines;
+    const void* __restrict__ W = p.wfft;
+    const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
+    const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
+    const Geometry& g = p.g;
+    const int lf = tid >> LOGTL;
+    const int jt = tid & (TL - 1);
+    const int lane = tid & 31;
+    const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
+    cx<T>* line_f = sm + lf * LS;
+    cx<T> v[16], pz[8];
+
+    if constexpr (OP == OP_FWD) {
+        // CONTIG only: I/O mapping == line-major mapping
+        fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+        const LineInfo L = linfo[lf];
+        const int kind = p.fkind;
         const T om = (T)p.out_mult;
-        const long long ob = Lio.out_off;
+        if (kind == FK_CFFT) {
+            if (!L.valid) return;
+            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + L.out_off + (long long)jt * g.out_st;
+            const long long step = (long long)TL * g.out_st;
+#pragma unroll
+            for (int r = 0; r < 16; ++r, po += step) *po = cscale<T>(v[r], om);
+            return;
+        }
+        fetch_mirror<T>(v, pz, jt, partner);
+        if (!L.valid) return;
         const long long os = g.out_st;
-        if (ik == IK_ICFFT) {
-            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
-            const long long step = (long long)TL * os;
+        if (kind == FK_RFFT) {
+            cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + L.out_off;
+            const T omh = om * (T)0.5;
 #pragma unroll
-            for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
-        } else {
-            const bool dct = ik != IK_IRFFT;
-            const bool dst = ik == IK_DST3;
-            T* const pb = reinterpret_cast<T*>(g.out) + ob;
-            if (!STRIDED) {
-                // output pairs (x_{2m}, x_{2m+1}), m = bio + TL it
-                T xv[32];
-#pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const int m = bio + it * TL;
-                    T x0, x1;
-                    if (dct) {
-                        const int pa = m, pbv = n - 1 - m;
-                        x0 = zr_io[2 * P(pa >> 1) + (pa & 1)];
-                        x1 = zr_io[2 * P(pbv >> 1) + (pbv & 1)];
-                        if (dst) x1 = -x1;
-                    } else {
-                        const cx<T> v = line_io[P(m)];
-                        x0 = v.x; x1 = v.y;
-                    }
-                    xv[2 * it] = x0 * om;
-                    xv[2 * it + 1] = x1 * om;
-                }
-                if (p.vec_out) {
-                    cx<T>* po = reinterpret_cast<cx<T>*>(pb) + bio;
-#pragma unroll
-                    for (int it = 0; it < 16; ++it) po[it * TL] = mkc<T>(xv[2 * it], xv[2 * it + 1]);
+            for (int r = 0; r < 8; ++r) {
+                const int q = jt + r * TL;
+                if (r == 0 && jt == 0) {
+                    const cx<T> z0 = v[0], zh = v[8];
+                    pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
+                    pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
+                    pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
                 } else {
-                    T* po = pb + (long long)(2 * bio) * os;
-                    const long long step = (long long)(2 * TL) * os;
-#pragma unroll
-                    for (int it = 0; it < 16; ++it, po += step) { po[0] = xv[2 * it]; po[os] = xv[2 * it + 1]; }
+                    const cx<T> tq = Wt[q];
+                    pb[(long long)q * os] = cscale<T>(rsplit2<T>(v[r], pz[r], tq), omh);
+                    pb[(long long)(M - q) * os] = cscale<T>(rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)), omh);
                 }
-            } else {
-                T* po = pb + (long long)bio * os;
-                const long long step = (long long)TL * os;
+            }
+        } else {
+            const bool dst = kind == FK_DST2;
+            T* const pb = reinterpret_cast<T*>(g.out) + L.out_off;
+            const long long s1 = dst ? -os : os;
+            T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;
 #pragma unroll
-                for (int it = 0; it < 32; ++it, po += step) {
-                    const int j = bio + it * TL;
-                    const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
-                    T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
-                    if (dst && (j & 1)) x = -x;
-                    *po = x * om;
+            for (int r = 0; r < 8; ++r) {
+                const int q = jt + r * TL;
+                if (r == 0 && jt == 0) {
+                    const cx<T> z0 = v[0], zh = v[8];
+                    const cx<T> wM = Ww[M];
+                    p0[0] = (T)2 * (z0.x + z0.y) * om;
+                    p0[(long long)M * s1] = (T)2 * (z0.x - z0.y) * wM.x * om;
+                    const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                    p0[(long long)HALF * s1] = U.x * om;
+                    p0[(long long)(n - HALF) * s1] = -U.y * om;
+                } else {
+                    const cx<T> tq = Wt[q], wq = Ww[q];
+                    const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
+                    const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)));
+                    p0[(long long)q * s1] = U1.x * om;
+                    p0[(long long)(n - q) * s1] = -U1.y * om;
+                    p0[(long long)(M - q) * s1] = U2.x * om;
+                    p0[(long long)(M + q) * s1] = -U2.y * om;
                 }
             }
         }
+        return;
+    } else {
+        if constexpr (OP == OP_MID) {
+            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            const int kind = p.fkind;
+            const Scaling& Sc = p.s;
+            const LineInfo L = linfo[lf];
+            const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+            const double cst = Sc.bscale * Sc.inv_np;
+            if (kind == FK_CFFT) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const int k = jt + r * TL;
+                    if (r == 0 && jt == 0) {
+                        if (cap) *Sc.dc_out = (double)v[0].x;
+                        v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
+                    } else {
+                        v[r] = cscale<T>(v[r], eig_factor_nz<T>(Sc, L, k, cst));
+                    }
+                }
+            } else {
+                fetch_mirror<T>(v, pz, jt, partner);
+                cx<T> half0 = mkc<T>(0, 0);
+                if (kind == FK_RFFT) {
+                    const double csth = cst * 0.5;
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const int q = jt + r * TL;
+                        if (r == 0 && jt == 0) {
+                            const cx<T> z0 = v[0], zh = v[8];
+                            T x0 = z0.x + z0.y, xM = z0.x - z0.y;
+                            if (cap) *Sc.dc_out = (double)x0;
+                            x0 *= eig_factor<T>(Sc, L, 0);
+                            xM *= eig_factor<T>(Sc, L, M);
+                            v[0] = mkc<T>(x0 + xM, x0 - xM);
+                            const cx<T> xh = cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), eig_factor<T>(Sc, L, HALF));
+                            half0 = rmerge<T>(xh, xh, Wt[HALF]);
+                        } else {
+                            const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                            const cx<T> xk = cscale<T>(rsplit2<T>(v[r], pz[r], tq), eig_factor_nz<T>(Sc, L, q, csth));
+                            const cx<T> xm = cscale<T>(rsplit2<T>(pz[r], v[r], tm), eig_factor_nz<T>(Sc, L, M - q, csth));
+                            v[r] = rmerge<T>(xk, xm, tq);
+                            pz[r] = rmerge<T>(xm, xk, tm);
+                        }
+                    }
+                } else {
+                    const bool dst = kind == FK_DST2;
+#define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const int q = jt + r * TL;
+                        if (r == 0 && jt == 0) {
+                            const cx<T> z0 = v[0], zh = v[8];
+                            const cx<T> wM = Ww[M];
+                            T X0 = (T)2 * (z0.x + z0.y);
+                            T XM = (T)2 * (z0.x - z0.y) * wM.x;
+                            if (cap && !dst) *Sc.dc_out = (double)X0;
+                            X0 *= eig_factor<T>(Sc, L, KPHYS(0));
+                            XM *= eig_factor<T>(Sc, L, KPHYS(M));
+                            const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                            v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                            const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                            const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
+                            const T Xa = (T)2 * U.x * eig_factor<T>(Sc, L, KPHYS(HALF));
+                            const T Xb = (T)-2 * U.y * eig_factor<T>(Sc, L, KPHYS(n - HALF));
+                            const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
+                            half0 = rmerge<T>(Vh, Vh, th);
+                        } else {
+                            const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                            const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
+                            const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
+                            const cx<T> U2 = cmul<T>(wm, rsplit2<T>(pz[r], v[r], tm));
+                            const cx<T> Y1 = mkc<T>(U1.x * eig_factor_nz<T>(Sc, L, KPHYS(q), cst),
+                                                    U1.y * eig_factor_nz<T>(Sc, L, KPHYS(n - q), cst));
+                            const cx<T> Y2 = mkc<T>(U2.x * eig_factor_nz<T>(Sc, L, KPHYS(M - q), cst),
+                                                    U2.y * eig_factor_nz<T>(Sc, L, KPHYS(M + q), cst));
+                            const cx<T> Vk = cmulc<T>(Y1, wq);
+                            const cx<T> Vm = cmulc<T>(Y2, wm);
+                            v[r] = rmerge<T>(Vk, Vm, tq);
+                            pz[r] = rmerge<T>(Vm, Vk, tm);
+                        }
+                    }
+#undef KPHYS
+                }
+                return_mirror<T>(v, pz, jt, partner, half0);
+            }
+        } else {
+            // OP_INV, real kinds: pre-processing from the placed spectrum
+            const int ik = p.ikind;
+            cx<T> half0 = mkc<T>(0, 0);
+            if (ik == IK_IRFFT) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int q = jt + r * TL;
+                    if (r == 0 && jt == 0) {
+                        const cx<T> x0 = line_f[P(0)], xM = line_f[P(M)], xh = line_f[P(HALF)];
+                        v[0] = rmerge<T>(x0, xM, mkc<T>(1, 0));
+                        half0 = rmerge<T>(xh, xh, Wt[HALF]);
+                    } else {
+                        const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
+                        const cx<T> tq = Wt[q];
+                        v[r] = rmerge<T>(xk, xm, tq);
+                        pz[r] = rmerge<T>(xm, xk, t_mirror<T>(tq));
+                    }
+                }
+            } else {
+                const T* zr = reinterpret_cast<const T*>(line_f);
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int q = jt + r * TL;
+                    if (r == 0 && jt == 0) {
+                        const T X0 = zr[PR(0)], XM = zr[PR(M)];
+                        const cx<T> wM = Ww[M];
+                        const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                        v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                        const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                        const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
+                        half0 = rmerge<T>(Vh, Vh, th);
+                    } else {
+                        const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
+                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                        const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
+                        const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
+                        v[r] = rmerge<T>(Vk, Vm, tq);
+                        pz[r] = rmerge<T>(Vm, Vk, tm);
+                    }
+                }
+            }
+            return_mirror<T>(v, pz, jt, partner, half0);
+        }
+        // inverse FFT from registers (its first write is preceded by a barrier,
+        // so the pre-processing reads above are complete)
+        fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+        compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
     }
 }
 
@@ -576,6 +844,12 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     bad |= place_nyquist<T, LOGM, OP>(p, Lio, line_io, bio);
     if (bad) *p.nonfinite = 1;
     __syncthreads();
+    if constexpr (S::TL <= 32 && !(OP == OP_FWD && STRIDED)) {
+        if (OP != OP_INV || p.ikind != IK_ICFFT) {
+            compute_store_reg<T, LOGM, STRIDED, OP>(p, linfo, sm);
+            return;
+        }
+    }
     compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);
 }
 
