@@ -284,9 +284,9 @@ __host__ __device__ __forceinline__ size_t linfo_bytes(int lines) {
 // eigenvalue factor for transform-axis index kt on line `L`
 template <typename T>
 __device__ __forceinline__ T eig_factor(const Scaling& s, const LineInfo& L, int kt) {
-    double lam = L.before + __ldg(&s.lam_t[kt]);
-    if (L.nafter > 0) lam += L.after1;
-    if (L.nafter > 1) lam += L.after2;
+    // absent axes contribute +0.0 (exact), so the adds are unconditional and
+    // the sum keeps the reference's axis order ((l0 + l1) + l2)
+    const double lam = ((L.before + __ldg(&s.lam_t[kt])) + L.after1) + L.after2;
     // bscale / lam via rcp.approx + two Newton steps (within 1 ulp of the IEEE
     // quotient of solver.py:158); the null mode (lam == 0) maps to 0
     double r;
