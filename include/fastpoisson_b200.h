@@ -22,6 +22,10 @@
  *   fp_transform_execute TransformPlan.execute_real/_complex transforms.py:157-172
  *   fp_last_error       exception message of the failing call
  *   fp_event_*          CUDA events behind SolveReport.timing (solver.py:215-228)
+ *   fp_plan_create_dist / fp_solve_phase / fp_dist_layout
+ *                       slab-decomposed solve over P ranks (the paper's MPI
+ *                       global transposes; the reorder seam
+ *                       "where a distributed exchange would slot in", reorder.py:7-8)
  *
  * Conventions
  *   - Arrays are C order (last axis contiguous) unless strides say otherwise;
@@ -169,6 +173,40 @@ FP_API fp_status fp_transform_execute(const fp_transform* t, int ndim, const int
                                       const void* in, int in_dtype, const int64_t* in_strides,
                                       void* out, int out_dtype, const int64_t* out_strides,
                                       void* stream);
+
+/* ---- slab decomposition over P ranks (axis 0 split; one all-to-all each way) ----
+ * Rank r owns planes [r*local_n0, (r+1)*local_n0) of axis 0 (local arrays are
+ * (local_n0, n1, n2) with any strides).  A solve is three phases with two
+ * all-to-alls of exchange_bytes between them, done by the caller (NCCL):
+ *   fp_solve_phase(plan, 0, rhs_local, ..., xbuf=send)    local transforms, packed send
+ *   all_to_all(send -> recv)                              equal blocks of exchange_bytes/P
+ *   fp_solve_phase(plan, 1, ..., xbuf=recv)               MID along the global axis 0
+ *   all_to_all(recv -> send)
+ *   fp_solve_phase(plan, 2, ..., out_local, xbuf=send)    local inverse transforms
+ * The exchange buffer holds (local_n0, exch_n1, exch_n2) elements with axis 1
+ * outermost (exch_n1 = n1 or its half spectrum, padded to a multiple of P).
+ * Only rank 0's dev_info receives the null coefficient. */
+typedef struct fp_dist_info {
+    int nranks, rank;
+    int64_t local_n0;       /* planes of axis 0 owned by this rank */
+    int64_t offset0;        /* first global plane */
+    int64_t exch_n1;        /* padded extent of axis 1 in the exchanged state */
+    int64_t true_n1;        /* its true extent */
+    int64_t exch_n2;        /* extent of axis 2 in the exchanged state (1 for 2D) */
+    int64_t block_n1;       /* exch_n1 / nranks */
+    int exch_complex;       /* exchanged state is complex (half spectrum) */
+    int r_axis;             /* periodic axis transformed as a real FFT (-1: none) */
+    int elem_bytes;
+    size_t exchange_bytes;  /* size of the send and of the receive buffer */
+} fp_dist_info;
+
+FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_dist_info* info); /* no device */
+FP_API fp_status fp_plan_create_dist(const fp_config* cfg, int device, int nranks, int rank, fp_plan** plan);
+FP_API fp_status fp_solve_phase(const fp_plan* plan, int phase,
+                                const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                                void* out, const int64_t* out_strides, void* xbuf,
+                                void* workspace, size_t workspace_bytes, void* stream,
+                                fp_solve_info* dev_info);
 
 /* CUDA event helpers for SolveReport.timing (phase_events of fp_solve). */
 FP_API fp_status fp_event_create(void** event);

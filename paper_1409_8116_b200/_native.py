@@ -58,6 +58,16 @@ class FpSolveInfo(Structure):
     _fields_ = [("dc", c_double), ("nonfinite", c_int32), ("reserved", c_int32)]
 
 
+class FpDistInfo(Structure):
+    _fields_ = [
+        ("nranks", c_int), ("rank", c_int),
+        ("local_n0", c_int64), ("offset0", c_int64),
+        ("exch_n1", c_int64), ("true_n1", c_int64), ("exch_n2", c_int64), ("block_n1", c_int64),
+        ("exch_complex", c_int), ("r_axis", c_int), ("elem_bytes", c_int),
+        ("exchange_bytes", c_size_t),
+    ]
+
+
 class FpSolveResult(Structure):
     _fields_ = [("removed_mean", c_double), ("timing", c_double * 3), ("total_seconds", c_double)]
 
@@ -91,6 +101,13 @@ SIGNATURES = {
         c_int,
         [c_void_p, c_int, POINTER(c_int64), c_int, c_void_p, c_int, POINTER(c_int64), c_void_p, c_int,
          POINTER(c_int64), c_void_p],
+    ),
+    "fp_dist_layout": (c_int, [POINTER(FpConfig), c_int, c_int, POINTER(FpDistInfo)]),
+    "fp_plan_create_dist": (c_int, [POINTER(FpConfig), c_int, c_int, c_int, POINTER(c_void_p)]),
+    "fp_solve_phase": (
+        c_int,
+        [c_void_p, c_int, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_void_p,
+         c_size_t, c_void_p, c_void_p],
     ),
     "fp_event_create": (c_int, [POINTER(c_void_p)]),
     "fp_event_destroy": (c_int, [c_void_p]),

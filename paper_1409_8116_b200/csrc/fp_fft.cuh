@@ -54,16 +54,18 @@ __device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo
         valid = ib < g.nb;
         if (!valid) ib = 0;
     }
+    const int iag = ia + g.a_off, ibg = ib + g.b_off;   // global line indices
+    if ((g.a_lim > 0 && iag >= g.a_lim) || (g.b_lim > 0 && ibg >= g.b_lim)) valid = false;
     L.valid = valid;
     L.in_off = (long long)ia * g.in_sa + (long long)ib * g.in_sb;
     L.out_off = (long long)ia * g.out_sa + (long long)ib * g.out_sb;
-    L.null_line = (ia == 0 && ib == 0);
+    L.null_line = (iag == 0 && ibg == 0);
     double before = 0.0, a1 = 0.0, a2 = 0.0;
     int nafter = 0;
     if (OP == OP_MID) {
         const bool ha = p.s.lam_a != nullptr, hb = p.s.lam_b != nullptr;
-        const double la = ha ? p.s.lam_a[ia] : 0.0;
-        const double lb = hb ? p.s.lam_b[ib] : 0.0;
+        const double la = (ha && valid) ? p.s.lam_a[iag] : 0.0;
+        const double lb = (hb && valid) ? p.s.lam_b[ibg] : 0.0;
         if (ha && p.s.pos_a < p.s.pos_t) before += la;
         if (hb && p.s.pos_b < p.s.pos_t) before += lb;
         if (ha && p.s.pos_a > p.s.pos_t) { a1 = la; nafter = 1; }
@@ -101,6 +103,29 @@ __device__ __forceinline__ void load_real(T* v, const T* base, long long st, boo
         for (int it = 0; it < CNT; ++it, base += step) v[it] = __ldg(base);
     }
 }
+// blocked transform axis (distributed exchange layout): row j at
+// (j >> lg) * hi + (j & (2^lg - 1)) * st
+template <typename T, int CNT, int STEP>
+__device__ __forceinline__ void load_real_blk(T* v, const T* line, int j0, long long st, long long hi, int lg,
+                                              bool valid) {
+    const int msk = (1 << lg) - 1;
+#pragma unroll
+    for (int it = 0; it < CNT; ++it) {
+        const int j = j0 + it * STEP;
+        v[it] = valid ? __ldg(line + (long long)(j >> lg) * hi + (long long)(j & msk) * st) : (T)0;
+    }
+}
+template <typename T, int CNT, int STEP>
+__device__ __forceinline__ void load_cx_blk(cx<T>* v, const cx<T>* line, int j0, long long st, long long hi, int lg,
+                                            bool valid) {
+    const int msk = (1 << lg) - 1;
+#pragma unroll
+    for (int it = 0; it < CNT; ++it) {
+        const int j = j0 + it * STEP;
+        v[it] = valid ? __ldg(line + (long long)(j >> lg) * hi + (long long)(j & msk) * st) : mkc<T>(0, 0);
+    }
+}
+
 // CONTIG real pairs (x_{2p}, x_{2p+1}), p = bio + TL it
 template <typename T, int TL>
 __device__ __forceinline__ void load_pairs(cx<T>* v, const T* line, long long st, bool valid, bool vec, int bio) {
@@ -156,7 +181,8 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
             }
         } else {
             T xr[32];
-            load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
+            if (p.g.blk_lg > 0) load_real_blk<T, 32, TL>(xr, rline, bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+            else load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
 #pragma unroll
             for (int it = 0; it < 32; ++it) {
                 const int j = bio + it * TL;
@@ -172,7 +198,8 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
             }
         }
     } else if (complex_input<OP>(p)) {
-        load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, !STRIDED && st == 1);
+        if (STRIDED && p.g.blk_lg > 0) load_cx_blk<T, 16, TL>(v, cline, bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+        else load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, !STRIDED && st == 1);
 #pragma unroll
         for (int it = 0; it < 16; ++it) {
             if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
@@ -234,6 +261,32 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
         const T om = (T)p.out_mult;
         const long long ob = Lio.out_off;
         const long long os = g.out_st;
+        if (STRIDED && g.blk_lg > 0) {
+            // distributed exchange layout: blocked transform axis
+            const int lg = g.blk_lg, msk = (1 << lg) - 1;
+            const long long hi = g.out_st_hi;
+            if (ik == IK_ICFFT) {
+                cx<T>* pb = reinterpret_cast<cx<T>*>(g.out) + ob;
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int k = bio + it * TL;
+                    pb[(long long)(k >> lg) * hi + (long long)(k & msk) * os] = cscale<T>(line_io[P(k)], om);
+                }
+            } else {
+                const bool dct = ik != IK_IRFFT;
+                const bool dst = ik == IK_DST3;
+                T* pb = reinterpret_cast<T*>(g.out) + ob;
+#pragma unroll
+                for (int it = 0; it < 32; ++it) {
+                    const int j = bio + it * TL;
+                    const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
+                    T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
+                    if (dst && (j & 1)) x = -x;
+                    pb[(long long)(j >> lg) * hi + (long long)(j & msk) * os] = x * om;
+                }
+            }
+            return;
+        }
         if (ik == IK_ICFFT) {
             cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
             const long long step = (long long)TL * os;

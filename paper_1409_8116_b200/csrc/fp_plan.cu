@@ -49,7 +49,7 @@ static fp_status fail(fp_status st, const std::string& msg) {
 
 namespace {
 
-enum Buf { B_RHS = 0, B_OUT = 1, B_RS = 2, B_CW = 3 };
+enum Buf { B_RHS = 0, B_OUT = 1, B_RS = 2, B_CW = 3, B_X = 4 };  // B_X: caller's exchange buffer (distributed)
 enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2 };
 enum Layout { LY_REAL = 0, LY_CPLX = 1 };  // state of the data in the buffer
 
@@ -73,6 +73,7 @@ struct PassT {
     DensePass dp;
     ScalePass sp;
     int a, b;            // other axes (-1 = dummy)
+    bool dist_mid;       // MID over the all-to-all receive layout (blocked axis 0)
 };
 
 // strides per axis for a buffer state (elements)
@@ -98,6 +99,13 @@ struct fp_plan {
     long long cpitch_last = 1;       // padded contiguous extent of the complex buffer
     bool need_cw = false, need_rs = false;
     bool mean_fix = false;           // exact arithmetic-mean removal (DCT-I axes)
+    // slab decomposition along axis 0
+    int nranks = 1, rank = 0;
+    long long a0 = 0;                // planes per rank
+    long long E1 = 0, B = 0;         // exchanged extent of axis 1 (padded to P) and per-peer block
+    long long e1 = 0, e2 = 1;        // true extents of axes 1, 2 in the exchanged state
+    bool x_cpx = false;              // exchanged state complex?
+    long long xs[3] = {0, 0, 0};     // exchange-buffer strides (send layout: axis 1 outermost)
     double bscale = 1.0;
     double np_prod = 1.0;
     double null_scale = 1.0;
@@ -291,17 +299,62 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
 
 }  // namespace
 
+// ----------------------------------------------------------------------------
+// Slab decomposition layout (device-free; shared by the planner and fp_dist_layout).
+struct DistLayout {
+    long long a0, e1, e2, E1, B;
+    int r_axis;
+    bool cpx;
+};
+
+static fp_status dist_layout(const fp_config* cfg, int nranks, DistLayout* L) {
+    const int d = cfg->ndim;
+    if (nranks < 1) return fail(FP_ERR_VALUE, "nranks must be >= 1");
+    if (nranks == 1) { *L = DistLayout{cfg->n[0], d > 1 ? cfg->n[1] : 1, d > 2 ? cfg->n[2] : 1, 0, 0, -1, false}; return FP_OK; }
+    if (d < 2) return fail(FP_ERR_UNSUPPORTED, "a 1D problem does not decompose over ranks");
+    if (!is_pow2(nranks) || cfg->n[0] % nranks) return fail(FP_ERR_UNSUPPORTED, "axis 0 must split evenly over a power-of-two rank count");
+    bool other_periodic = false;
+    for (int a = 1; a < d; ++a) other_periodic |= cfg->bc[a] == FP_BC_PERIODIC;
+    if (other_periodic && cfg->bc[0] != FP_BC_PERIODIC)
+        return fail(FP_ERR_UNSUPPORTED, "distributed solve: with periodic axes other than 0, axis 0 must be periodic");
+    if (fft_length(cfg->bc[0], cfg->kind[0], cfg->n[0], cfg->bc[0] == FP_BC_PERIODIC && !other_periodic) == 0)
+        return fail(FP_ERR_UNSUPPORTED, "distributed solve: axis 0 must be on the FFT engine (power-of-two length)");
+    for (int a = 0; a < d; ++a)
+        if (cfg->bc[a] == FP_BC_NEUMANN && cfg->kind[a] == FP_GRID_REGULAR)
+            return fail(FP_ERR_UNSUPPORTED, "distributed solve: DCT-I axes (exact mean removal) not supported");
+    // forward order without axis 0: real axes descending, then periodic descending
+    int r_axis = -1;
+    for (int a = d - 1; a >= 1; --a) if (cfg->bc[a] == FP_BC_PERIODIC && r_axis < 0) r_axis = a;
+    if (r_axis < 0 && cfg->bc[0] == FP_BC_PERIODIC) r_axis = 0;
+    DistLayout l{};
+    l.a0 = cfg->n[0] / nranks;
+    l.r_axis = r_axis;
+    l.cpx = r_axis > 0;
+    l.e1 = cfg->n[1];
+    l.e2 = d > 2 ? cfg->n[2] : 1;
+    if (r_axis == 1) l.e1 = cfg->n[1] / 2 + 1;
+    if (r_axis == 2) l.e2 = cfg->n[2] / 2 + 1;
+    l.E1 = (l.e1 + nranks - 1) / nranks * nranks;
+    l.B = l.E1 / nranks;
+    *L = l;
+    return FP_OK;
+}
+
 // ============================================================================
 extern "C" {
 
 FP_API int fp_abi_version(void) { return FP_ABI_VERSION; }
 FP_API const char* fp_last_error(void) { return g_err.c_str(); }
 
-FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out) {
+static fp_status build_plan(const fp_config* cfg, int device, int nranks, int rank, fp_plan** out) {
     if (!out) return fail(FP_ERR_VALUE, "plan out-pointer is NULL");
     *out = nullptr;
     fp_status st = validate(cfg);
     if (st != FP_OK) return st;
+    if (rank < 0 || rank >= nranks) return fail(FP_ERR_VALUE, "rank out of range");
+    DistLayout DL{};
+    if ((st = dist_layout(cfg, nranks, &DL)) != FP_OK) return st;
+    const bool dist = nranks > 1;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(FP_ERR_CUDA, "no CUDA device available (the solve path has no CPU fallback)");
@@ -311,6 +364,8 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
     fp_plan* P = new fp_plan();
     P->device = device;
     P->cfg = *cfg;
+    P->nranks = nranks;
+    P->rank = rank;
     const int d = cfg->ndim;
     P->ndim = d;
     P->f32 = cfg->precision == FP_F32;
@@ -342,9 +397,21 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
     }
 
     // forward order: real axes descending, then periodic axes descending
+    // (distributed: axis 0 -- the decomposed one -- always last, i.e. the MID axis)
     std::vector<int> order;
-    for (int a = d - 1; a >= 0; --a) if (cfg->bc[a] != FP_BC_PERIODIC) order.push_back(a);
-    for (int a = d - 1; a >= 0; --a) if (cfg->bc[a] == FP_BC_PERIODIC) { if (P->r_axis < 0) P->r_axis = a; order.push_back(a); }
+    const int amin = dist ? 1 : 0;
+    for (int a = d - 1; a >= amin; --a) if (cfg->bc[a] != FP_BC_PERIODIC) order.push_back(a);
+    for (int a = d - 1; a >= amin; --a) if (cfg->bc[a] == FP_BC_PERIODIC) { if (P->r_axis < 0) P->r_axis = a; order.push_back(a); }
+    if (dist) {
+        if (P->r_axis < 0 && cfg->bc[0] == FP_BC_PERIODIC) P->r_axis = 0;
+        order.push_back(0);
+        P->a0 = DL.a0;
+        P->n[0] = DL.a0;             // local extents from here on; cfg->n keeps the global ones
+        P->e1 = DL.e1; P->e2 = DL.e2; P->E1 = DL.E1; P->B = DL.B; P->x_cpx = DL.cpx;
+        // send layout: axis 1 outermost -> peer q's block (axis-1 rows [qB,(q+1)B)) is contiguous
+        if (d == 3) { P->xs[0] = DL.e2; P->xs[1] = DL.a0 * DL.e2; P->xs[2] = 1; }
+        else { P->xs[0] = 1; P->xs[1] = DL.a0; }
+    }
     P->middle = order.back();
     for (int a = 0; a < 3; ++a) P->cext[a] = P->n[a];
     if (P->r_axis >= 0) P->cext[P->r_axis] = P->n[P->r_axis] / 2 + 1;
@@ -510,8 +577,9 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
         const bool rf = t == P->r_axis;
         const bool in_cpx = complex_state;
         const bool out_cpx = complex_state || rf;
-        const int dst = out_cpx ? B_CW : realbuf;
-        if (out_cpx) P->need_cw = true; else P->need_rs = true;
+        int dst = out_cpx ? B_CW : realbuf;
+        if (dist && i + 2 == order.size()) dst = B_X;   // pack for the all-to-all
+        else if (out_cpx) P->need_cw = true; else P->need_rs = true;
         if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_FWD, in_cpx, out_cpx, cur, dst, 0));
         else P->passes.push_back(make_dense(t, true, in_cpx, out_cpx, cur, dst, 0));
         if (rf) complex_state = true;
@@ -522,7 +590,15 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
         const int t = P->middle;
         const bool rf = t == P->r_axis;
         const int dst = only_middle ? B_OUT : cur;
-        if (Mx[t] > 0) {
+        if (dist) {
+            // MID over the receive layout: global axis 0 in P blocks of a0 planes
+            PassT mid = make_fft(t, OP_MID, complex_state, complex_state, B_X, B_X, 1);
+            mid.dist_mid = true;
+            if (d == 3) { mid.fp.g.na = (int)DL.B; mid.fp.g.nb = (int)DL.e2; }
+            else { mid.fp.g.na = 1; mid.fp.g.nb = (int)DL.B; }
+            fft_tile_shape(mid.fp, P->f32, complex_state, mid.fp.g.na, mid.fp.g.nb);
+            P->passes.push_back(mid);
+        } else if (Mx[t] > 0) {
             P->passes.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
         } else if (!rf) {
             // dense forward, scale, dense inverse on the same buffer
@@ -551,8 +627,10 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
         const bool in_cpx = complex_state;
         const bool out_cpx = complex_state && !rf;
         const bool last = i == 0;
-        const int dst = last ? B_OUT : (out_cpx ? B_CW : (in_cpx ? realbuf : cur));
+        int dst = last ? B_OUT : (out_cpx ? B_CW : (in_cpx ? realbuf : cur));
+        if (!last && cur == B_X) dst = out_cpx ? B_CW : realbuf;   // unpack out of the exchange buffer
         if (!out_cpx && !last) P->need_rs = true;
+        if (out_cpx && !last) P->need_cw = true;
         if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_INV, in_cpx, out_cpx, cur, dst, 2));
         else P->passes.push_back(make_dense(t, false, in_cpx, out_cpx, cur, dst, 2));
         if (rf) complex_state = false;
@@ -561,6 +639,10 @@ FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** out)
     // the first pass checks finiteness of the rhs (solver.py:201-202)
     *out = P;
     return FP_OK;
+}
+
+FP_API fp_status fp_plan_create(const fp_config* cfg, int device, fp_plan** plan) {
+    return build_plan(cfg, device, 1, 0, plan);
 }
 
 FP_API fp_status fp_plan_destroy(fp_plan* plan) {
@@ -628,12 +710,16 @@ FP_API fp_status fp_solve(const fp_plan* P, const void* rhs, int rhs_dtype, cons
                        dev_info, phase_events, nullptr);
 }
 
-FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
-                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
-                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
-                             void* const* pass_events) {
+static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                            void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
+                            void* stream, fp_solve_info* dev_info, void* const* phase_events,
+                            void* const* pass_events, void* xbuf, int ph_lo, int ph_hi) {
     if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
-    if (!rhs || !out) return fail(FP_ERR_VALUE, "rhs/out is NULL");
+    const bool need_rhs = ph_lo == 0, need_out = ph_hi == 2;
+    if ((need_rhs && !rhs) || (need_out && !out)) return fail(FP_ERR_VALUE, "rhs/out is NULL");
+    if (P->nranks > 1 && !xbuf) return fail(FP_ERR_VALUE, "distributed plan: exchange buffer is NULL");
+    if (!rhs) { rhs = out ? out : xbuf; rhs_dtype = P->f32 ? FP_F32 : FP_F64; }
+    if (!out) out = const_cast<void*>(rhs);
     if (rhs_dtype != FP_F64 && rhs_dtype != FP_F32) return fail(FP_ERR_VALUE, "rhs dtype must be f64 or f32");
     const int d = P->ndim;
     long long dense_r[3];
@@ -653,13 +739,13 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
         return fail(FP_ERR_VALUE, "workspace too small: need " + std::to_string(need) + " bytes");
     DeviceGuard dg(P->device);
     cudaStream_t st = (cudaStream_t)stream;
-    if (dev_info) CUDA_TRY(cudaMemsetAsync(dev_info, 0, sizeof(fp_solve_info), st));
+    if (dev_info && ph_lo == 0) CUDA_TRY(cudaMemsetAsync(dev_info, 0, sizeof(fp_solve_info), st));
 
     void* cw = workspace;
     void* rsb = out_dense ? out : (void*)((char*)workspace + cw_bytes(P));
     // rhs in another precision: cast once into the real scratch (dense, plan-typed)
     const int plan_fp = P->f32 ? FP_F32 : FP_F64;
-    if (rhs_dtype != plan_fp) {
+    if (rhs_dtype != plan_fp && ph_lo == 0) {
         CastPass cp{};
         for (int k = 0; k < 3; ++k) { cp.ext[k] = 1; cp.st[k] = 0; }
         for (int a = 0; a < d; ++a) { cp.ext[3 - d + a] = (int)P->n[a]; cp.st[3 - d + a] = rs_s[a]; }
@@ -679,6 +765,7 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
             case B_RHS: return const_cast<void*>(rhs);
             case B_OUT: return out;
             case B_RS: return rsb;
+            case B_X: return xbuf;
             default: return cw;
         }
     };
@@ -686,6 +773,7 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
         if (b == B_RHS) { for (int a = 0; a < 3; ++a) s[a] = rs_s[a]; return; }
         if (b == B_OUT) { for (int a = 0; a < 3; ++a) s[a] = os_s[a]; return; }
         if (b == B_RS) { for (int a = 0; a < 3; ++a) s[a] = out_dense ? os_s[a] : dense_r[a]; return; }
+        if (b == B_X) { for (int a = 0; a < 3; ++a) s[a] = P->xs[a]; return; }
         (void)layout;
         for (int a = 0; a < 3; ++a) s[a] = cw_s[a];
     };
@@ -701,6 +789,7 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
     bool first = true;
     for (size_t i = 0; i < P->passes.size(); ++i) {
         const PassT& T = P->passes[i];
+        if (T.phase < ph_lo || T.phase > ph_hi) continue;
         while (ev && phase < T.phase) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
         if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[i], st));
         long long si[3], so[3];
@@ -723,6 +812,17 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
         if (T.engine == EN_FFT) {
             FftPass p = T.fp;
             g.na = p.g.na; g.nb = p.g.nb;
+            if (T.dist_mid) {
+                // receive layout [source rank][axis-1 block][a0 planes][axis 2]:
+                // global plane j = src * a0 + i  ->  src * (B * a0 * e2) + i * e2
+                int lg = 0;
+                while ((1LL << lg) < P->a0) ++lg;
+                g.blk_lg = lg;
+                g.in_st_hi = g.out_st_hi = P->B * P->xs[1];
+                if (lg == 0) { g.in_st = g.out_st = g.in_st_hi; }
+                if (d == 3) { g.a_off = (int)(P->rank * P->B); g.a_lim = (int)P->e1; }
+                else { g.b_off = (int)(P->rank * P->B); g.b_lim = (int)P->e1; }
+            }
             p.g = g;
             p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
             p.s.dc_out = dev_info ? &dev_info->dc : nullptr;
@@ -758,7 +858,7 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
         if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
         first = false;
     }
-    if (P->mean_fix) {
+    if (P->mean_fix && ph_hi == 2) {
         MeanPass m{};
         for (int k = 0; k < 3; ++k) { m.ext[k] = 1; m.st[k] = 0; }
         for (int a = 0; a < d; ++a) { m.ext[3 - d + a] = (int)P->n[a]; m.st[3 - d + a] = os_s[a]; }
@@ -770,6 +870,52 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
     if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[P->passes.size()], st));
     while (ev && phase < 3) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
     return FP_OK;
+}
+
+FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
+                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
+                             void* const* pass_events) {
+    if (P && P->nranks > 1) return fail(FP_ERR_VALUE, "distributed plan: use fp_solve_phase");
+    return solve_impl(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
+                      dev_info, phase_events, pass_events, nullptr, 0, 2);
+}
+
+FP_API fp_status fp_solve_phase(const fp_plan* P, int phase, const void* rhs, int rhs_dtype,
+                                const int64_t* rhs_strides, void* out, const int64_t* out_strides,
+                                void* xbuf, void* workspace, size_t workspace_bytes, void* stream,
+                                fp_solve_info* dev_info) {
+    if (phase < 0 || phase > 2) return fail(FP_ERR_VALUE, "phase must be 0 (forward), 1 (middle) or 2 (backward)");
+    return solve_impl(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
+                      dev_info, nullptr, nullptr, xbuf, phase, phase);
+}
+
+FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_dist_info* info) {
+    if (!info) return fail(FP_ERR_VALUE, "NULL argument");
+    fp_status st = validate(cfg);
+    if (st != FP_OK) return st;
+    if (rank < 0 || rank >= nranks) return fail(FP_ERR_VALUE, "rank out of range");
+    DistLayout L{};
+    if ((st = dist_layout(cfg, nranks, &L)) != FP_OK) return st;
+    std::memset(info, 0, sizeof(*info));
+    info->nranks = nranks;
+    info->rank = rank;
+    info->local_n0 = nranks > 1 ? L.a0 : cfg->n[0];
+    info->offset0 = (int64_t)rank * info->local_n0;
+    info->exch_n1 = nranks > 1 ? L.E1 : 0;
+    info->true_n1 = nranks > 1 ? L.e1 : 0;
+    info->exch_n2 = nranks > 1 ? L.e2 : 0;
+    info->block_n1 = nranks > 1 ? L.B : 0;
+    info->exch_complex = L.cpx;
+    info->r_axis = L.r_axis;
+    const int rb = cfg->precision == FP_F32 ? 4 : 8;
+    info->elem_bytes = (L.cpx ? 2 : 1) * rb;
+    info->exchange_bytes = nranks > 1 ? (size_t)L.a0 * L.E1 * L.e2 * info->elem_bytes : 0;
+    return FP_OK;
+}
+
+FP_API fp_status fp_plan_create_dist(const fp_config* cfg, int device, int nranks, int rank, fp_plan** plan) {
+    return build_plan(cfg, device, nranks, rank, plan);
 }
 
 FP_API fp_status fp_removed_mean(const fp_plan* P, const fp_solve_info* h, double* rm) {

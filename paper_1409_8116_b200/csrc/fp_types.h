@@ -39,6 +39,15 @@ struct Geometry {
     const void* in;
     void* out;
     int in_type, out_type;
+    // distributed exchange layout (slab decomposition):
+    // element j of a line at (j >> blk_lg) * st_hi + (j & (2^blk_lg - 1)) * st
+    // when blk_lg > 0 (the all-to-all's source-rank blocks along axis 0;
+    // zero-initialized geometry = plain stride)
+    int blk_lg;
+    long long in_st_hi, out_st_hi;
+    // global index of the line axes = local + off; lines with global >= lim
+    // (lim > 0) are padding (not loaded, not stored, no eigenvalue lookup)
+    int a_off, a_lim, b_off, b_lim;
 };
 
 // Eigenvalue scaling of the middle pass (solver.py:151-159,221).  The factor

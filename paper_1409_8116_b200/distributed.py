@@ -1,0 +1,171 @@
+"""Slab-decomposed Poisson solve over a torch.distributed process group.
+
+The reference package runs in one process (SPEC.md:11 drops distribution); the
+paper's library decomposed the grid over MPI ranks with global transposes
+(PAPER.md:409-447), and the reference keeps "the seam where a distributed
+exchange would slot in" (reorder.py:7-8).  This module is that exchange on
+B200s: one process per GPU, axis 0 split into slabs, and per solve
+
+    phase 0  local transforms along axes d-1..1, packed into the send buffer
+             (axis 1 outermost, so every peer's block is contiguous)
+    all-to-all (NCCL over NVLink / NVSwitch)
+    phase 1  fused forward / eigenvalue divide / inverse along the global axis 0
+             (the kernel reads the receive layout directly: no unpack pass)
+    all-to-all back
+    phase 2  local inverse transforms into the caller's output slab
+
+Phases are kernels of the native library (``fp_solve_phase``); the exchanges
+are ``torch.distributed.all_to_all_single`` on byte tensors.  ``backend`` is
+pluggable so the orchestration (layout contract, exchange pattern, reductions)
+can be exercised on CPU with gloo in the test tier.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device as dv
+from . import _native as nat
+from .solver import SolveReport, SolverConfig, _config_struct
+
+
+def dist_layout(config: SolverConfig, nranks: int, rank: int) -> nat.FpDistInfo:
+    """Layout of the decomposition (device-free; the native planner's own rules)."""
+    lib = nat.load()
+    cfg, keep = _config_struct(config)
+    info = nat.FpDistInfo()
+    nat.check(lib.fp_dist_layout(ctypes.byref(cfg), int(nranks), int(rank), ctypes.byref(info)))
+    del keep
+    return info
+
+
+class NativeBackend:
+    """The three solve phases on the local GPU through the C ABI."""
+
+    def __init__(self, config: SolverConfig, nranks: int, rank: int, device=None):
+        t = dv.torch()
+        self.config = config
+        self.device = dv.require_cuda(device)
+        self._lib = nat.load()
+        cfg, keep = _config_struct(config)
+        h = ctypes.c_void_p()
+        nat.check(self._lib.fp_plan_create_dist(ctypes.byref(cfg), self.device.index, int(nranks), int(rank),
+                                                ctypes.byref(h)))
+        del keep
+        self._handle = h
+        self.info = dist_layout(config, nranks, rank)
+        self.local_shape = (int(self.info.local_n0),) + tuple(config.shape[1:])
+        self.dtype = dv.torch_dtype(config.dtype)
+        nbytes = int(self.info.exchange_bytes)
+        self.send = t.empty(nbytes, dtype=t.uint8, device=self.device)
+        self.recv = t.empty(nbytes, dtype=t.uint8, device=self.device)
+        ws = ctypes.c_size_t()
+        nat.check(self._lib.fp_plan_workspace_bytes(self._handle, 1, ctypes.byref(ws)))
+        self._ws_dense = int(ws.value)
+        nat.check(self._lib.fp_plan_workspace_bytes(self._handle, 0, ctypes.byref(ws)))
+        self._ws_strided = int(ws.value)
+        self.status = t.zeros(16, dtype=t.uint8, device=self.device)
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None:
+            try:
+                self._lib.fp_plan_destroy(h)
+            except Exception:  # pragma: no cover
+                pass
+
+    def _workspace(self, out_dense):
+        t = dv.torch()
+        n = self._ws_dense if out_dense else self._ws_strided
+        return t.empty(max(n, 1), dtype=t.uint8, device=self.device), n
+
+    def _call(self, phase, rhs, out, xbuf):
+        t = dv.torch()
+        out_dense = out is None or out.is_contiguous()
+        ws, nws = self._workspace(out_dense)
+        rhs_ptr = rhs.data_ptr() if rhs is not None else None
+        rhs_dt = dv.fp_dtype_of_torch(rhs.dtype) if rhs is not None else 0
+        rhs_st = nat.strides_array(rhs.stride()) if rhs is not None else None
+        out_ptr = out.data_ptr() if out is not None else None
+        out_st = nat.strides_array(out.stride()) if out is not None else None
+        rc = self._lib.fp_solve_phase(self._handle, phase, rhs_ptr, rhs_dt, rhs_st, out_ptr, out_st,
+                                      xbuf.data_ptr(), ws.data_ptr(), nws, dv.stream_handle(self.device),
+                                      self.status.data_ptr())
+        nat.check(rc)
+        return ws
+
+    def forward(self, rhs_local, out_local):
+        # the real scratch of phase 0 may live in `out_local` (dense outputs)
+        self._ws0 = self._call(0, rhs_local, out_local, self.send)
+
+    def middle(self):
+        self._ws1 = self._call(1, None, None, self.recv)
+
+    def backward(self, out_local):
+        self._ws2 = self._call(2, None, out_local, self.send)
+
+    def read_status(self):
+        """(raw null coefficient, non-finite flag) of this rank, as float64 tensor on the device."""
+        t = dv.torch()
+        dc = self.status[:8].view(t.float64)
+        nf = self.status[8:12].view(t.int32).to(t.float64)
+        return t.cat([dc, nf])
+
+    def new_output(self):
+        t = dv.torch()
+        return t.empty(self.local_shape, dtype=self.dtype, device=self.device)
+
+
+class DistributedSolverPlan:
+    """Drop-in ``SolverPlan`` semantics for one global grid split over the ranks.
+
+    ``solve(rhs_local, out_local=None)`` takes this rank's slab (planes
+    ``local_slice`` of axis 0) and returns this rank's slab of the solution plus
+    the global ``SolveReport`` (identical on every rank).
+    """
+
+    def __init__(self, config: SolverConfig, group=None, device=None, backend=None):
+        import torch.distributed as dist
+
+        self.config = config
+        self.group = group
+        self.nranks = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.backend = backend if backend is not None else NativeBackend(config, self.nranks, self.rank, device)
+        self.info = self.backend.info
+        self.local_shape = tuple(self.backend.local_shape)
+        off = int(self.info.offset0)
+        self.local_slice = slice(off, off + int(self.info.local_n0))
+        # removed_mean = dc / (prod n_periodic * null_scale) (solver.py:218-220)
+        from .solver import _ONES_NULL_COEFF
+        from .transforms import transform_pair_for
+        import math
+
+        pairs = [transform_pair_for(g.bc, g.kind) for g in config.grids]
+        self._np = math.prod(g.n for g in config.grids if g.bc.value == "periodic")
+        self._null = math.prod(_ONES_NULL_COEFF[p.forward](g.n) for g, p in zip(config.grids, pairs)) if config.singular else 1.0
+
+    def solve(self, rhs_local, out_local=None):
+        import torch.distributed as dist
+
+        t = dv.torch()
+        if tuple(rhs_local.shape) != self.local_shape:
+            raise ValueError(f"local rhs extents {tuple(rhs_local.shape)} do not match {self.local_shape}")
+        if out_local is None:
+            out_local = self.backend.new_output()
+        be = self.backend
+        be.forward(rhs_local, out_local)
+        dist.all_to_all_single(be.recv, be.send, group=self.group)
+        be.middle()
+        dist.all_to_all_single(be.send, be.recv, group=self.group)
+        be.backward(out_local)
+        status = be.read_status()
+        dist.all_reduce(status, op=dist.ReduceOp.SUM, group=self.group)
+        dc, nonfinite = float(status[0]), float(status[1])
+        if nonfinite > 0:
+            raise ValueError("rhs contains non-finite values")
+        rep = SolveReport(mode=self.config.mode, periodic_axes=self.config.periodic_axes)
+        rep.removed_mean = (dc / self._np) / self._null if self.config.singular else 0.0
+        return out_local, rep

@@ -51,6 +51,27 @@ _ONES_NULL_COEFF = {
 }
 
 
+def _config_struct(config, tables=None):
+    """fp_config for a SolverConfig, carrying the host mirror's numpy eigenvalue
+    tables (bit-identical to the reference's, eigenvalues.py:51-83)."""
+    if tables is None:
+        tables = [eigenvalue_table(g, config.approximation) for g in config.grids]
+    cfg = nat.FpConfig()
+    cfg.ndim = config.dims
+    keep = []
+    for a, g in enumerate(config.grids):
+        cfg.n[a] = g.n
+        cfg.length[a] = float(g.length)
+        cfg.bc[a] = _BC_ID[g.bc]
+        cfg.kind[a] = _KIND_ID[g.kind]
+        tab = np.ascontiguousarray(tables[a].values, dtype=np.float64)
+        keep.append(tab)
+        cfg.eig[a] = tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    cfg.approx = _APPROX_ID[config.approximation]
+    cfg.precision = nat.FP_F32 if config.precision == "single" else nat.FP_F64
+    return cfg, keep
+
+
 @dataclass(frozen=True)
 class SolverConfig:
     """Grid specification per axis plus the approximation to diagonalize (solver.py:65-119)."""
@@ -168,19 +189,7 @@ class SolverPlan:
         self._info = info
 
     def _create_native(self):
-        cfg = nat.FpConfig()
-        cfg.ndim = self.config.dims
-        keep = []
-        for a, g in enumerate(self.config.grids):
-            cfg.n[a] = g.n
-            cfg.length[a] = float(g.length)
-            cfg.bc[a] = _BC_ID[g.bc]
-            cfg.kind[a] = _KIND_ID[g.kind]
-            tab = np.ascontiguousarray(self.tables[a].values, dtype=np.float64)
-            keep.append(tab)
-            cfg.eig[a] = tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        cfg.approx = _APPROX_ID[self.config.approximation]
-        cfg.precision = nat.FP_F32 if self.config.precision == "single" else nat.FP_F64
+        cfg, keep = _config_struct(self.config, self.tables)
         h = ctypes.c_void_p()
         nat.check(self._lib.fp_plan_create(ctypes.byref(cfg), self._device.index, ctypes.byref(h)))
         del keep
