@@ -10,8 +10,9 @@ so no explicit flush is needed between steps).
 
 --impl reference times the reference algorithm on the host cores (the oracle
 port in oracle/, which calls scipy.fft exactly like the reference) on the same
-workload.  Under torchrun every rank runs its own replica solve (no data-path
-collective): "replicas" scaling, see DESIGN.md.
+workload.  Under torchrun (N > 1) the ranks solve ONE global grid together:
+slab decomposition along axis 0, two NCCL all-to-alls per solve (strong
+scaling), reported against both the HBM and the NVLink rooflines.
 """
 
 from __future__ import annotations
@@ -196,6 +197,110 @@ def measure_e2e(plan, rhs, shape, tdt, n_pts, s, args, ws, dist, dev):
     return e2e
 
 
+def run_dist(args, ws, rank, local):
+    """N > 1: ONE global grid split over the ranks (slab decomposition, NCCL all-to-all)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1409_8116_b200 as fp  # noqa: F401
+    from paper_1409_8116_b200 import _device as dv
+    from paper_1409_8116_b200.distributed import DistributedSolverPlan
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    config, case = make_config(args.config)
+    plan = DistributedSolverPlan(config, device=dev)
+    shape = config.shape
+    n_pts = int(np.prod(shape))
+    s = config.dtype.itemsize
+    tdt = dv.torch_dtype(config.dtype)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    rhs = torch.randn(plan.local_shape, dtype=tdt, device=dev, generator=gen)
+    out = torch.empty_like(rhs)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 1)):
+        plan.solve_async(rhs, out)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(stream)
+    for _ in range(args.steps):
+        plan.solve_async(rhs, out)
+    ev[1].record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clocks = sampler.stop()
+    tt = torch.tensor([ev[0].elapsed_time(ev[1])], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tt.item())
+    ms_step = elapsed_ms / args.steps
+    value = args.steps / (elapsed_ms * 1e-3)          # solves/s of the one global grid
+    hbm_peak, peak_src = peaks()
+    import ctypes
+    from paper_1409_8116_b200 import _native as nat
+
+    pinfo = nat.FpPlanInfo()
+    nat.check(nat.load().fp_plan_info_get(plan.backend._handle, ctypes.byref(pinfo)))
+    launches = int(pinfo.num_passes) * args.steps   # this rank's kernels (NCCL kernels not counted)
+    b_alg = (2 * len(shape) - 1) * 2 * n_pts * s
+    xbytes = int(plan.info.exchange_bytes)
+    nvl_bytes = 2 * xbytes * (ws - 1) / ws             # sent per GPU per solve (two all-to-alls)
+    nvl_peak = 900.0
+    roofline = {
+        "bound": "hbm+nvlink",
+        "achieved": b_alg / ws / (ms_step * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+        "frac": b_alg / ws / (ms_step * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+        "kernel": "whole distributed solve per GPU (B_alg / P)", "peak_source": peak_src,
+        "nvlink": {"bytes_per_gpu_per_solve": nvl_bytes, "achieved": nvl_bytes / (ms_step * 1e-3) / 1e9,
+                   "peak": nvl_peak, "unit": "GB/s", "frac": nvl_bytes / (ms_step * 1e-3) / 1e9 / nvl_peak,
+                   "peak_source": "nominal NVLink 5 per direction per GPU"},
+    }
+    # e2e: each rank's slab from pinned host memory, solve, slab back (public distributed API)
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(plan.local_shape, dtype=tdt, pin_memory=True)
+        host_in.copy_(rhs)
+        host_out = torch.empty(plan.local_shape, dtype=tdt, pin_memory=True)
+        e2e_steps = max(1, min(args.steps, 10))
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            d_in = host_in.to(dev, non_blocking=True)
+            o, rep = plan.solve(d_in)
+            host_out.copy_(o)
+        e2e_dt = time.perf_counter() - t0
+        tt = torch.tensor([e2e_dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_dt = float(tt.item())
+        e2e = {"value": e2e_steps / e2e_dt, "unit": "solves/s",
+               "h2d_bytes_per_step": n_pts * s, "d2h_bytes_per_step": n_pts * s,
+               "path": "DistributedSolverPlan.solve(slab from pinned host) + slab D2H, every rank"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": config.dtype.name.replace("float", "f"),
+            "data": "synthetic (seeded N(0,1) slabs generated on device)",
+            "config": {"workload": WORKLOADS[args.config], "grid": list(shape),
+                       "parallelism": f"slab decomposition along axis 0 over {ws} GPUs, NCCL all-to-all",
+                       "l2": "inputs larger than L2; no flush"},
+            "gpoints_per_s": value * n_pts / 1e9,
+            "roofline": roofline,
+            "cpu_baseline": None,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args, ws, rank, local):
     import ctypes
 
@@ -353,6 +458,9 @@ def main():
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+        return
+    if ws > 1:
+        run_dist(args, ws, rank, local)
         return
     run_ours(args, ws, rank, local)
 

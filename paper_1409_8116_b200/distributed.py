@@ -147,10 +147,10 @@ class DistributedSolverPlan:
         self._np = math.prod(g.n for g in config.grids if g.bc.value == "periodic")
         self._null = math.prod(_ONES_NULL_COEFF[p.forward](g.n) for g, p in zip(config.grids, pairs)) if config.singular else 1.0
 
-    def solve(self, rhs_local, out_local=None):
+    def solve_async(self, rhs_local, out_local=None):
+        """Enqueue one distributed solve (kernels + NCCL all-to-alls) without synchronizing."""
         import torch.distributed as dist
 
-        t = dv.torch()
         if tuple(rhs_local.shape) != self.local_shape:
             raise ValueError(f"local rhs extents {tuple(rhs_local.shape)} do not match {self.local_shape}")
         if out_local is None:
@@ -161,6 +161,13 @@ class DistributedSolverPlan:
         be.middle()
         dist.all_to_all_single(be.send, be.recv, group=self.group)
         be.backward(out_local)
+        return out_local
+
+    def solve(self, rhs_local, out_local=None):
+        import torch.distributed as dist
+
+        out_local = self.solve_async(rhs_local, out_local)
+        be = self.backend
         status = be.read_status()
         dist.all_reduce(status, op=dist.ReduceOp.SUM, group=self.group)
         dc, nonfinite = float(status[0]), float(status[1])
