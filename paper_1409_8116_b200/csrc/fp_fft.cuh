@@ -145,6 +145,32 @@ __device__ __forceinline__ void load_pairs(cx<T>* v, const T* line, long long st
 }
 
 // ----------------------------------------------------------------------------
+// STRIDED tiles: thread (column c, block b) owns the contiguous rows
+// j = 32 b + i (real lines, n = 2M rows) or k = 16 b + i (complex, M rows), so
+// the W lanes of a warp still read/write 128-byte row segments while every
+// padded shared-memory address is a per-thread base plus a compile-time offset:
+//   complex k = 16b + i          -> P(k)  = 17 b + i
+//   real (half-FFT packing) j    -> 2 P(j >> 1) + (j & 1) = 34 b + i
+//   Makhoul v index of j (DCT):  even i = 2m: pv = 16 b + m           -> 16 b + 2 (b >> 1) + m
+//                                odd  i = 2m+1: pv = n-1-16b-m         -> base_o - m,
+//                                base_o = 16 K - 1 + 2 ((K-1) >> 1), K = n/16 - b
+//   PR(k), k = 32 b + i          -> 33 b + i;  PR(n-1-k) -> 33 K' - 2 - i, K' = n/32 - b
+struct RowBlk {
+    int cpx17, r34, mk_e, mk_o, pr, prr;
+    __device__ __forceinline__ RowBlk(int b, int n) {
+        cpx17 = 17 * b;
+        r34 = 34 * b;
+        mk_e = 16 * b + 2 * (b >> 1);
+        const int K = n / 16 - b;
+        mk_o = 16 * K - 1 + 2 * ((K - 1) >> 1);
+        pr = 33 * b;
+        prr = 33 * (n / 32 - b) - 2;
+    }
+    // real-tile index of row j = 32 b + i under the Makhoul reordering
+    __device__ __forceinline__ int makhoul(int i) const { return (i & 1) ? (mk_o - (i >> 1)) : (mk_e + (i >> 1)); }
+};
+
+// ----------------------------------------------------------------------------
 // placement: line values -> padded complex tile in the layout the FFT expects
 // (Makhoul reordering / half-length packing for real kinds).  Returns the
 // non-finite flag of the values it read.
@@ -181,29 +207,38 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
             }
         } else {
             T xr[32];
-            if (p.g.blk_lg > 0) load_real_blk<T, 32, TL>(xr, rline, bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
-            else load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
+            if (p.g.blk_lg > 0) load_real_blk<T, 32, 1>(xr, rline, 32 * bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+            else load_real<T, 32, 1>(xr, rline + (long long)(32 * bio) * st, st, Lio.valid);
+            const RowBlk rb(bio, n);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 32; ++it) {
-                const int j = bio + it * TL;
-                T x = xr[it];
-                if (chk) bad |= !finite_t(x);
-                int pv;
-                if (kind == FK_RFFT) pv = j;
-                else {
-                    pv = (j & 1) ? (n - 1 - (j >> 1)) : (j >> 1);
-                    if (kind == FK_DST2 && (j & 1)) x = -x;
-                }
-                zr_io[2 * P(pv >> 1) + (pv & 1)] = x;
+                for (int it = 0; it < 32; ++it) bad |= !finite_t(xr[it]);
+            }
+            if (kind == FK_RFFT) {
+#pragma unroll
+                for (int it = 0; it < 32; ++it) zr_io[rb.r34 + it] = xr[it];
+            } else {
+                const bool dst = kind == FK_DST2;
+#pragma unroll
+                for (int it = 0; it < 32; ++it) zr_io[rb.makhoul(it)] = (dst && (it & 1)) ? -xr[it] : xr[it];
             }
         }
     } else if (complex_input<OP>(p)) {
-        if (STRIDED && p.g.blk_lg > 0) load_cx_blk<T, 16, TL>(v, cline, bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
-        else load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, !STRIDED && st == 1);
+        if constexpr (STRIDED) {
+            if (p.g.blk_lg > 0) load_cx_blk<T, 16, 1>(v, cline, 16 * bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+            else load_cx<T, 16, 1>(v, cline + (long long)(16 * bio) * st, st, Lio.valid, false);
 #pragma unroll
-        for (int it = 0; it < 16; ++it) {
-            if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-            line_io[P(bio + it * TL)] = v[it];
+            for (int it = 0; it < 16; ++it) {
+                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+                line_io[17 * bio + it] = v[it];
+            }
+        } else {
+            load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, st == 1);
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+                line_io[P(bio + it * TL)] = v[it];
+            }
         }
     } else {
         // DCT-III / DST-III: real spectrum of n = 2M entries
@@ -219,12 +254,12 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
             }
         } else {
             T xr[32];
-            load_real<T, 32, TL>(xr, rline + (long long)bio * st, st, Lio.valid);
+            load_real<T, 32, 1>(xr, rline + (long long)(32 * bio) * st, st, Lio.valid);
+            const RowBlk rb(bio, n);
 #pragma unroll
             for (int it = 0; it < 32; ++it) {
-                const int k = bio + it * TL;
                 if (chk) bad |= !finite_t(xr[it]);
-                zr_io[PR(dst ? n - 1 - k : k)] = xr[it];
+                zr_io[dst ? rb.prr - it : rb.pr + it] = xr[it];
             }
         }
     }
@@ -288,10 +323,16 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
             return;
         }
         if (ik == IK_ICFFT) {
-            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
-            const long long step = (long long)TL * os;
+            if constexpr (STRIDED) {
+                cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)(16 * bio) * os;
 #pragma unroll
-            for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
+                for (int it = 0; it < 16; ++it, po += os) *po = cscale<T>(line_io[17 * bio + it], om);
+            } else {
+                cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)bio * os;
+                const long long step = (long long)TL * os;
+#pragma unroll
+                for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
+            }
         } else {
             const bool dct = ik != IK_IRFFT;
             const bool dst = ik == IK_DST3;
@@ -326,15 +367,17 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                     for (int it = 0; it < 16; ++it, po += step) { po[0] = xv[2 * it]; po[os] = xv[2 * it + 1]; }
                 }
             } else {
-                T* po = pb + (long long)bio * os;
-                const long long step = (long long)TL * os;
+                T* po = pb + (long long)(32 * bio) * os;
+                const RowBlk rb(bio, n);
+                if (dct) {
 #pragma unroll
-                for (int it = 0; it < 32; ++it, po += step) {
-                    const int j = bio + it * TL;
-                    const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
-                    T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
-                    if (dst && (j & 1)) x = -x;
-                    *po = x * om;
+                    for (int it = 0; it < 32; ++it, po += os) {
+                        const T x = zr_io[rb.makhoul(it)] * om;
+                        *po = (dst && (it & 1)) ? -x : x;
+                    }
+                } else {
+#pragma unroll
+                    for (int it = 0; it < 32; ++it, po += os) *po = zr_io[rb.r34 + it] * om;
                 }
             }
         }
@@ -399,6 +442,79 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
         if constexpr (OP == OP_FWD) {
             const int kind = p.fkind;
             const T om = (T)p.out_mult;
+            if constexpr (STRIDED) {
+                // thread (column, block b) owns quads q = 8 b + i, i < 8 (CFFT: k = 16 b + i):
+                //   P(q) = 8 b + (b >> 1) + i;  P(M - q) = 8 K2 - i + (i ? (K2 - 1) >> 1 : K2 >> 1), K2 = M/8 - b
+                if (Lio.valid) {
+                    const long long ob = Lio.out_off;
+                    const long long os = g.out_st;
+                    const int b = bio;
+                    const int pq0 = 8 * b + (b >> 1);
+                    const int K2 = M / 8 - b;
+                    const int pm0 = 8 * K2 + (K2 >> 1), pm1 = 8 * K2 + ((K2 - 1) >> 1);
+#define PM(I) ((I) == 0 ? pm0 : (pm1 - (I)))
+                    if (kind == FK_CFFT) {
+                        cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)(16 * b) * os;
+#pragma unroll
+                        for (int it = 0; it < 16; ++it, po += os) *po = cscale<T>(line_io[17 * b + it], om);
+                    } else if (kind == FK_RFFT) {
+                        cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + ob;
+                        cx<T>* pq = pb + (long long)(8 * b) * os;
+                        cx<T>* pm = pb + (long long)(M - 8 * b) * os;
+                        const T omh = om * (T)0.5;
+#pragma unroll
+                        for (int it = 0; it < 8; ++it, pq += os, pm -= os) {
+                            const int q = 8 * b + it;
+                            if (it == 0 && b == 0) {
+                                const cx<T> z0 = line_io[P(0)];
+                                pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
+                                pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
+                                const cx<T> zh = line_io[P(HALF)];
+                                pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
+                            } else {
+                                const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
+                                const cx<T> tq = Wt[q];
+                                *pq = cscale<T>(rsplit2<T>(zk, zm, tq), omh);
+                                *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
+                            }
+                        }
+                    } else {
+                        const bool dst = kind == FK_DST2;
+                        T* const pb = reinterpret_cast<T*>(g.out) + ob;
+                        const long long s1 = dst ? -os : os;
+                        T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;
+                        T* pa = p0 + (long long)(8 * b) * s1;
+                        T* pn = p0 + (long long)(n - 8 * b) * s1;
+                        T* pm = p0 + (long long)(M - 8 * b) * s1;
+                        T* pp = p0 + (long long)(M + 8 * b) * s1;
+#pragma unroll
+                        for (int it = 0; it < 8; ++it, pa += s1, pn -= s1, pm -= s1, pp += s1) {
+                            const int q = 8 * b + it;
+                            if (it == 0 && b == 0) {
+                                const cx<T> z0 = line_io[P(0)];
+                                const cx<T> wM = Ww[M];
+                                p0[0] = (T)2 * (z0.x + z0.y) * om;
+                                p0[(long long)M * s1] = (T)2 * (z0.x - z0.y) * wM.x * om;
+                                const cx<T> zh = line_io[P(HALF)];
+                                const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                                p0[(long long)HALF * s1] = U.x * om;
+                                p0[(long long)(n - HALF) * s1] = -U.y * om;
+                            } else {
+                                const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
+                                const cx<T> tq = Wt[q], wq = Ww[q];
+                                const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
+                                const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
+                                *pa = U1.x * om;
+                                *pn = -U1.y * om;
+                                *pm = U2.x * om;
+                                *pp = -U2.y * om;
+                            }
+                        }
+                    }
+#undef PM
+                }
+                return;
+            }
             if (Lio.valid) {
                 const long long ob = Lio.out_off;
                 const long long os = g.out_st;
