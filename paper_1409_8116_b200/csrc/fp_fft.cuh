@@ -12,6 +12,8 @@
 //     line), STRIDED = column-major (lanes walk across the W adjacent lines so
 //     each row segment of W elements is one coalesced access).
 #pragma once
+#include <type_traits>
+
 #include "fp_common.cuh"
 
 namespace fpb {
@@ -191,18 +193,21 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
         const int kind = p.fkind;
         if (!STRIDED) {
             load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const int pi = bio + it * TL;
-                T x0 = v[it].x, x1 = v[it].y;
-                if (chk) bad |= !(finite_t(x0) && finite_t(x1));
-                if (kind == FK_RFFT) {
-                    line_io[P(pi)] = mkc<T>(x0, x1);
-                } else {
-                    if (kind == FK_DST2) x1 = -x1;
-                    const int pa = pi, pb = n - 1 - pi;  // Makhoul: v_pi = x_j, v_{n-1-pi} = x_{j+1}
-                    zr_io[2 * P(pa >> 1) + (pa & 1)] = x0;
-                    zr_io[2 * P(pb >> 1) + (pb & 1)] = x1;
+                for (int it = 0; it < 16; ++it) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+            }
+            if (kind == FK_RFFT) {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) line_io[P(bio + it * TL)] = v[it];
+            } else {
+                // Makhoul: v_pi = x_j, v_{n-1-pi} = x_{j+1} (DST-II: sign-alternated input)
+                const T sgn = (kind == FK_DST2) ? (T)-1 : (T)1;
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int pa = bio + it * TL, pb = n - 1 - pa;
+                    zr_io[2 * P(pa >> 1) + (pa & 1)] = v[it].x;
+                    zr_io[2 * P(pb >> 1) + (pb & 1)] = sgn * v[it].y;
                 }
             }
         } else {
@@ -218,48 +223,68 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
 #pragma unroll
                 for (int it = 0; it < 32; ++it) zr_io[rb.r34 + it] = xr[it];
             } else {
-                const bool dst = kind == FK_DST2;
+                const T sgn = (kind == FK_DST2) ? (T)-1 : (T)1;
 #pragma unroll
-                for (int it = 0; it < 32; ++it) zr_io[rb.makhoul(it)] = (dst && (it & 1)) ? -xr[it] : xr[it];
+                for (int it = 0; it < 32; ++it) zr_io[rb.makhoul(it)] = (it & 1) ? sgn * xr[it] : xr[it];
             }
         }
     } else if (complex_input<OP>(p)) {
         if constexpr (STRIDED) {
             if (p.g.blk_lg > 0) load_cx_blk<T, 16, 1>(v, cline, 16 * bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
             else load_cx<T, 16, 1>(v, cline + (long long)(16 * bio) * st, st, Lio.valid, false);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-                line_io[17 * bio + it] = v[it];
+                for (int it = 0; it < 16; ++it) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
             }
+#pragma unroll
+            for (int it = 0; it < 16; ++it) line_io[17 * bio + it] = v[it];
         } else {
             load_cx<T, 16, TL>(v, cline + (long long)bio * st, st, Lio.valid, st == 1);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-                line_io[P(bio + it * TL)] = v[it];
+                for (int it = 0; it < 16; ++it) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
             }
+#pragma unroll
+            for (int it = 0; it < 16; ++it) line_io[P(bio + it * TL)] = v[it];
         }
     } else {
         // DCT-III / DST-III: real spectrum of n = 2M entries
         const bool dst = p.ikind == IK_DST3;
         if (!STRIDED) {
             load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const int k = 2 * (bio + it * TL);
-                if (chk) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
-                zr_io[PR(dst ? n - 1 - k : k)] = v[it].x;
-                zr_io[PR(dst ? n - 2 - k : k + 1)] = v[it].y;
+                for (int it = 0; it < 16; ++it) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
+            }
+            if (dst) {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int kk = 2 * (bio + it * TL);
+                    zr_io[PR(n - 1 - kk)] = v[it].x;
+                    zr_io[PR(n - 2 - kk)] = v[it].y;
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int kk = 2 * (bio + it * TL);
+                    zr_io[PR(kk)] = v[it].x;
+                    zr_io[PR(kk + 1)] = v[it].y;
+                }
             }
         } else {
             T xr[32];
             load_real<T, 32, 1>(xr, rline + (long long)(32 * bio) * st, st, Lio.valid);
             const RowBlk rb(bio, n);
+            if (chk) {
 #pragma unroll
-            for (int it = 0; it < 32; ++it) {
-                if (chk) bad |= !finite_t(xr[it]);
-                zr_io[dst ? rb.prr - it : rb.pr + it] = xr[it];
+                for (int it = 0; it < 32; ++it) bad |= !finite_t(xr[it]);
+            }
+            if (dst) {
+#pragma unroll
+                for (int it = 0; it < 32; ++it) zr_io[rb.prr - it] = xr[it];
+            } else {
+#pragma unroll
+                for (int it = 0; it < 32; ++it) zr_io[rb.pr + it] = xr[it];
             }
         }
     }
@@ -340,21 +365,21 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
             if (!STRIDED) {
                 // output pairs (x_{2m}, x_{2m+1}), m = bio + TL it
                 T xv[32];
+                if (dct) {
+                    const T sgn = dst ? -om : om;
 #pragma unroll
-                for (int it = 0; it < 16; ++it) {
-                    const int m = bio + it * TL;
-                    T x0, x1;
-                    if (dct) {
-                        const int pa = m, pbv = n - 1 - m;
-                        x0 = zr_io[2 * P(pa >> 1) + (pa & 1)];
-                        x1 = zr_io[2 * P(pbv >> 1) + (pbv & 1)];
-                        if (dst) x1 = -x1;
-                    } else {
-                        const cx<T> v = line_io[P(m)];
-                        x0 = v.x; x1 = v.y;
+                    for (int it = 0; it < 16; ++it) {
+                        const int pa = bio + it * TL, pbv = n - 1 - pa;
+                        xv[2 * it] = zr_io[2 * P(pa >> 1) + (pa & 1)] * om;
+                        xv[2 * it + 1] = zr_io[2 * P(pbv >> 1) + (pbv & 1)] * sgn;
                     }
-                    xv[2 * it] = x0 * om;
-                    xv[2 * it + 1] = x1 * om;
+                } else {
+#pragma unroll
+                    for (int it = 0; it < 16; ++it) {
+                        const cx<T> v = line_io[P(bio + it * TL)];
+                        xv[2 * it] = v.x * om;
+                        xv[2 * it + 1] = v.y * om;
+                    }
                 }
                 if (p.vec_out) {
                     cx<T>* po = reinterpret_cast<cx<T>*>(pb) + bio;
@@ -370,11 +395,9 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                 T* po = pb + (long long)(32 * bio) * os;
                 const RowBlk rb(bio, n);
                 if (dct) {
+                    const T sgn = dst ? -om : om;   // DST-III: odd outputs negated
 #pragma unroll
-                    for (int it = 0; it < 32; ++it, po += os) {
-                        const T x = zr_io[rb.makhoul(it)] * om;
-                        *po = (dst && (it & 1)) ? -x : x;
-                    }
+                    for (int it = 0; it < 32; ++it, po += os) *po = zr_io[rb.makhoul(it)] * ((it & 1) ? sgn : om);
                 } else {
 #pragma unroll
                     for (int it = 0; it < 32; ++it, po += os) *po = zr_io[rb.r34 + it] * om;
