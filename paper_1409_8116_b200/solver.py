@@ -336,6 +336,82 @@ class SolverPlan:
         _copy_to_host(out_t, out_arr)
         return out_arr, report
 
+    def solve_batch(self, rhs_seq, out_seq=None):
+        """Solve a sequence of host right-hand sides, streaming them through the GPU.
+
+        Equivalent to ``[self.solve(r, o) for r, o in zip(rhs_seq, out_seq)]``
+        (same results, same errors), but the host->device copy of solve i+1, the
+        kernels of solve i and the device->host copy of solve i-1 run
+        concurrently on three CUDA streams (PCIe is full duplex), with two device
+        buffers per direction.  Pinned host arrays give the full copy bandwidth.
+        Returns a list of ``(solution, SolveReport)``.
+        """
+        t = dv.torch()
+        rhs_list = [np.asarray(as_array(r)) for r in rhs_seq]
+        if out_seq is None:
+            out_list = [np.empty(self.shape, dtype=self.dtype) for _ in rhs_list]
+        else:
+            out_list = [as_array(o) for o in out_seq]
+        if len(out_list) != len(rhs_list):
+            raise ValueError("rhs and out sequences differ in length")
+        for r, o in zip(rhs_list, out_list):
+            if tuple(r.shape) != self.shape:
+                raise ValueError(f"rhs extents {tuple(r.shape)} do not match plan extents {self.shape}")
+            if tuple(o.shape) != self.shape:
+                raise ValueError(f"solution extents {tuple(o.shape)} do not match plan extents {self.shape}")
+        dev = self._device
+        tdt = dv.torch_dtype(self.dtype)
+        s_in, s_run, s_out = t.cuda.Stream(dev), t.cuda.Stream(dev), t.cuda.Stream(dev)
+        d_in = [None, None]
+        d_out = [t.empty(self.shape, dtype=tdt, device=dev) for _ in range(2)]
+        infos = [t.zeros(16, dtype=t.uint8, device=dev) for _ in rhs_list]
+        ev_in = [t.cuda.Event() for _ in range(2)]
+        ev_run = [t.cuda.Event() for _ in range(2)]
+        ev_out = [t.cuda.Event() for _ in range(2)]
+        events = [_Events(self._lib) for _ in rhs_list]
+        host_out = [None] * len(rhs_list)
+        keep = []
+        for i, r in enumerate(rhs_list):
+            b = i & 1
+            if r.dtype not in (np.float32, np.float64):
+                r = r.astype(self.dtype)
+            rt = t.from_numpy(np.ascontiguousarray(r))
+            with t.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_run[b])          # buffer b consumed by solve i-2
+                d_in[b] = rt.to(dev, non_blocking=True)
+                d_in[b].record_stream(s_run)
+                ev_in[b].record(s_in)
+            with t.cuda.stream(s_run):
+                s_run.wait_event(ev_in[b])
+                if i >= 2:
+                    s_run.wait_event(ev_out[b])         # d_out[b] drained by the copy of solve i-2
+                ws = self._launch(d_in[b], d_out[b], infos[i], events[i], stream=s_run.cuda_stream)
+                keep.append(ws)
+                ev_run[b].record(s_run)
+            with t.cuda.stream(s_out):
+                s_out.wait_event(ev_run[b])
+                o = out_list[i]
+                if (o.flags.c_contiguous and o.flags.writeable and o.dtype == self.dtype):
+                    dst = t.from_numpy(o)
+                else:
+                    dst = t.empty(self.shape, dtype=tdt, pin_memory=True)
+                dst.copy_(d_out[b], non_blocking=True)
+                host_out[i] = dst
+                ev_out[b].record(s_out)
+        s_out.synchronize()
+        s_run.synchronize()
+        results = []
+        for i, o in enumerate(out_list):
+            info_host = nat.FpSolveInfo.from_buffer_copy(infos[i].cpu().numpy().tobytes())
+            if info_host.nonfinite:
+                raise ValueError(f"rhs {i} contains non-finite values")
+            if host_out[i].data_ptr() != o.ctypes.data:
+                o[...] = host_out[i].numpy()
+            results.append((o, self._report(info_host, events[i])))
+        del keep
+        return results
+
     def solve_async(self, rhs_t, out_t=None, info_t=None):
         """Enqueue a device solve without synchronizing (throughput path).
 

@@ -346,3 +346,19 @@ def test_laplacian_aid_device_matches_host(torch_cuda, rng):
     np.testing.assert_allclose(d, h, atol=1e-12 * np.abs(h).max())
     case = orc.Case([(9, 1.0, "neumann", "regular"), (7, 1.0, "neumann", "regular")], "fd2")
     np.testing.assert_allclose(h, orc.laplacian(case, x), atol=1e-12 * np.abs(h).max())
+
+
+def test_solve_batch_matches_individual_solves(torch_cuda, rng):
+    plan = _plan(BC.NEUMANN, GK.STAGGERED, (64, 32, 32))
+    rhs = [rng.standard_normal((64, 32, 32)) for _ in range(5)]
+    single = [plan.solve(r) for r in rhs]
+    outs = [np.empty((64, 32, 32)) for _ in range(5)]
+    batch = plan.solve_batch(rhs, outs)
+    for (a, ra), (b, rb), o in zip(single, batch, outs):
+        np.testing.assert_array_equal(a, b)
+        assert b is o
+        assert ra.removed_mean == rb.removed_mean
+    bad = [r.copy() for r in rhs[:3]]
+    bad[1][0, 0, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        plan.solve_batch(bad)
