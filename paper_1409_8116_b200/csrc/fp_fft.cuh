@@ -28,6 +28,16 @@ template <int LOGM> struct Shape {
     static constexpr int LS = ((M + M / 16 + 1) & 1) ? (M + M / 16 + 1) : (M + M / 16 + 2);
 };
 
+// shared-memory line stride (complex elements).  With one line per warp
+// (TL >= 32) the stride only shapes the strided I/O, so the planner picks it
+// per tile (FftPass::ls) to keep those accesses bank-conflict free; otherwise
+// it is the compile-time odd stride the multi-line FFT stages need.
+template <typename T, int LOGM, bool STRIDED>
+__device__ __forceinline__ int line_stride(const FftPass& p) {
+    if constexpr (STRIDED && Shape<LOGM>::TL >= 32) return p.ls;
+    else return Shape<LOGM>::LS;
+}
+
 // does this (op, kind) read complex lines?
 template <int OP>
 __device__ __forceinline__ bool complex_input(const FftPass& p) {
@@ -306,7 +316,8 @@ __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& 
 template <typename T, int LOGM, bool STRIDED>
 __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
     using S = Shape<LOGM>;
-    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, LS = S::LS;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
+    const int LS = line_stride<T, LOGM, STRIDED>(p);
     constexpr int n = 2 * M;
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
@@ -441,7 +452,8 @@ __device__ __forceinline__ T eig_factor_nz(const Scaling& s, const LineInfo& L, 
 template <typename T, int LOGM, bool STRIDED, int OP>
 __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
     using S = Shape<LOGM>;
-    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, LS = S::LS;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF;
+    const int LS = line_stride<T, LOGM, STRIDED>(p);
     constexpr bool fwd_in = OP != OP_INV;
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
@@ -804,7 +816,8 @@ __device__ __forceinline__ void return_mirror(cx<T>* v, const cx<T>* pz, int jt,
 template <typename T, int LOGM, bool STRIDED, int OP>
 __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
     using S = Shape<LOGM>;
-    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, LS = S::LS;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF;
+    const int LS = line_stride<T, LOGM, STRIDED>(p);
     constexpr int n = 2 * M;
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
@@ -1031,7 +1044,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     const int lio = STRIDED ? (tid & (p.lines - 1)) : (tid >> S::LOGTL);
     const int bio = STRIDED ? (tid >> p.logLines) : (tid & (S::TL - 1));
     const LineInfo Lio = linfo[lio];
-    cx<T>* line_io = sm + lio * S::LS;
+    cx<T>* line_io = sm + lio * line_stride<T, LOGM, STRIDED>(p);
     bool bad = place_tile<T, LOGM, STRIDED, OP>(p, Lio, line_io, bio);
     bad |= place_nyquist<T, LOGM, OP>(p, Lio, line_io, bio);
     if (bad) *p.nonfinite = 1;
@@ -1045,11 +1058,117 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);
 }
 
+// ----------------------------------------------------------------------------
+// Pipelined STRIDED path: persistent CTAs, two transform tiles.  The loads of
+// tile i+1 are cp.async copies of single elements (4/8/16 bytes) straight into
+// their padded slots of the second tile -- the Makhoul / half-FFT placement is
+// just the destination address -- while tile i is transformed and stored.
+// (DST kinds need a sign flip on load and the first pass needs the
+// non-finite check: both stay on fft_pass_kernel.)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* dst, const void* src) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <typename T, int LOGM, int OP>
+__device__ __forceinline__ void issue_tile_async(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M;
+    const int LS = line_stride<T, LOGM, true>(p);
+    constexpr int n = 2 * M;
+    const int tid = threadIdx.x;
+    const int lio = tid & (p.lines - 1);
+    const int b = tid >> p.logLines;
+    const LineInfo L = linfo[lio];
+    if (!L.valid) return;
+    const Geometry& g = p.g;
+    cx<T>* line = sm + lio * LS;
+    T* zr = reinterpret_cast<T*>(line);
+    const long long st = g.in_st;
+    const bool blk = g.blk_lg > 0;
+    const int lg = g.blk_lg, msk = (1 << (lg > 0 ? lg : 0)) - 1;
+    auto row_off = [&](int j) -> long long {
+        return blk ? (long long)(j >> lg) * g.in_st_hi + (long long)(j & msk) * st : (long long)j * st;
+    };
+    const bool cin = complex_input<OP>(p);
+    if (cin) {
+        const cx<T>* src = reinterpret_cast<const cx<T>*>(g.in) + L.in_off;
+#pragma unroll
+        for (int it = 0; it < 16; ++it)
+            cp_async_elem<sizeof(cx<T>)>(line + 17 * b + it, src + row_off(16 * b + it));
+        if (OP == OP_INV && p.ikind == IK_IRFFT && b == 0)
+            cp_async_elem<sizeof(cx<T>)>(line + P(M), src + (long long)M * st);
+    } else {
+        const T* src = reinterpret_cast<const T*>(g.in) + L.in_off;
+        const RowBlk rb(b, n);
+        if (OP == OP_INV) {             // DCT-III: real spectrum in the PR layout
+#pragma unroll
+            for (int it = 0; it < 32; ++it) cp_async_elem<sizeof(T)>(zr + rb.pr + it, src + (long long)(32 * b + it) * st);
+        } else if (p.fkind == FK_RFFT) {
+#pragma unroll
+            for (int it = 0; it < 32; ++it) cp_async_elem<sizeof(T)>(zr + rb.r34 + it, src + row_off(32 * b + it));
+        } else {                        // DCT-II: Makhoul reordering
+#pragma unroll
+            for (int it = 0; it < 32; ++it) cp_async_elem<sizeof(T)>(zr + rb.makhoul(it), src + row_off(32 * b + it));
+        }
+    }
+}
+
+template <typename T, int LOGM, int OP>
+__global__ void __launch_bounds__(512) fft_pass_spipe(const FftPass p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using S = Shape<LOGM>;
+    const unsigned lib = (unsigned)linfo_bytes(p.lines);
+    const unsigned zb = (unsigned)p.lines * (unsigned)line_stride<T, LOGM, true>(p) * (unsigned)sizeof(cx<T>);
+    // buffer k: line table at smem_raw + k*lib, tile at smem_raw + 2*lib + k*zb
+    int tile = blockIdx.x;
+    if (tile >= p.tiles) return;
+    setup_lines<true, OP>(p, tile, reinterpret_cast<LineInfo*>(smem_raw));
+    __syncthreads();
+    issue_tile_async<T, LOGM, OP>(p, reinterpret_cast<LineInfo*>(smem_raw), reinterpret_cast<cx<T>*>(smem_raw + 2 * lib));
+    cp_async_commit_group();
+    for (unsigned k = 0; tile < p.tiles; tile += gridDim.x, k ^= 1u) {
+        const int next = tile + gridDim.x;
+        LineInfo* lc = reinterpret_cast<LineInfo*>(smem_raw + k * lib);
+        LineInfo* ln = reinterpret_cast<LineInfo*>(smem_raw + (k ^ 1u) * lib);
+        cx<T>* zc = reinterpret_cast<cx<T>*>(smem_raw + 2 * lib + k * zb);
+        cx<T>* zn = reinterpret_cast<cx<T>*>(smem_raw + 2 * lib + (k ^ 1u) * zb);
+        if (next < p.tiles) setup_lines<true, OP>(p, next, ln);
+        __syncthreads();   // ln written; zn free (the previous tile's compute is done)
+        if (next < p.tiles) issue_tile_async<T, LOGM, OP>(p, ln, zn);
+        cp_async_commit_group();
+        cp_async_wait_prev();  // this thread's copies of `tile` have landed
+        __syncthreads();       // ... and everybody's
+        if constexpr (S::TL <= 32 && OP != OP_FWD) {
+            if (OP != OP_INV || p.ikind != IK_ICFFT) {
+                compute_store_reg<T, LOGM, true, OP>(p, lc, zc);
+                continue;
+            }
+        }
+        compute_store<T, LOGM, true, OP>(p, lc, zc);
+    }
+}
+
+template <typename T, int L, int OPV>
+inline FftKernelFn spipe_fn(bool strided) {
+    if constexpr (OPV == OP_MID) return nullptr;   // the MID step is not pipelined
+    else return strided ? (FftKernelFn)fft_pass_spipe<T, L, OPV> : (FftKernelFn) nullptr;
+}
+
 }  // namespace fpb
 
-// (a persistent, TMA/cp.async double-buffered variant was measured slower on
-// B200 -- its staging tiles cut residency to 1-2 CTAs/SM -- and was removed)
-#define FP_FFT_PIPE_FN(T, L, s, OPV) ((FftKernelFn) nullptr)
+// (an earlier persistent variant that staged raw rows through TMA/cp.async
+// buffers and then re-placed them was slower -- its staging tiles cut residency
+// to 1-2 CTAs/SM; fft_pass_spipe copies straight into the transform tile)
+#define FP_FFT_PIPE_FN(T, L, s, OPV) spipe_fn<T, L, OPV>(s)
 
 #define FP_FFT_PICK(NAME, T, LO, HI)                                                                  \
     namespace fpb {                                                                                   \

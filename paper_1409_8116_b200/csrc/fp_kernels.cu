@@ -225,6 +225,25 @@ cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* ou
 
 // ----------------------------------------------------------------------------
 // launchers (host)
+// Line stride of a strided tile (complex elements, >= M + M/16 + 1).  With
+// TL >= 32 each warp owns one line, so only the strided placement / store
+// pattern  lio * LS + 17 b + i  (lio = tid % W, b = tid / W) constrains it:
+// E elements fill one 128-byte wavefront (E = 16 for complex fp32, 8 for
+// complex fp64), and LS = E/W (mod E) maps the E threads of a wavefront onto
+// distinct banks.  Real operands (and short lines) keep the odd stride.
+int strided_line_stride(const FftPass& p, bool f32) {
+    const int base = p.M + p.M / 16 + 1;
+    const int odd = base | 1;
+    if (p.family != FAM_STRIDED || p.logM < 9) return odd;
+    const bool cin = (p.op == OP_INV) ? (p.ikind == IK_ICFFT || p.ikind == IK_IRFFT) : (p.fkind == FK_CFFT);
+    const int E = f32 ? 16 : 8;
+    if (!cin || p.lines > E) return odd;
+    const int want = (E / p.lines) % E;
+    int ls = base;
+    while (ls % E != want) ++ls;
+    return ls;
+}
+
 size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes) {
     return linfo_bytes(p.lines) + (size_t)p.lines * p.ls * 2 * real_bytes;
 }
@@ -235,6 +254,18 @@ static FftKernelFn pick_fft(int logM, bool strided, int op, bool pipe) {
     return logM <= 8 ? pick_fft_f_lo(logM, strided, op, pipe) : pick_fft_f_hi(logM, strided, op, pipe);
 }
 
+// Opt in to the full 227 KB per CTA AND ask for the max-shared carveout: left to
+// itself the driver sizes the L1/shared split for ONE resident CTA of the
+// kernel's request, capping e.g. 70 KB tiles at 1 CTA/SM instead of 3.
+static cudaError_t allow_smem(const void* fn) {
+    if (!fn) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    const char* v = getenv("FP_CARVEOUT");   // percent, or unset = driver default
+    if (!v || !*v) return cudaSuccess;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
+}
+
 static cudaError_t set_smem_attr() {
     static bool done = false;
     if (done) return cudaSuccess;
@@ -243,14 +274,19 @@ static cudaError_t set_smem_attr() {
         for (int s = 0; s < 2; ++s)
             for (int op = 0; op < 3; ++op)
                 for (int pp = 0; pp < 2; ++pp) {
-                    FftKernelFn fd = pick_fft<double>(l, s, op, pp), ff = pick_fft<float>(l, s, op, pp);
-                    if (fd && (e = cudaFuncSetAttribute(fd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-                    if (ff && (e = cudaFuncSetAttribute(ff, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+                    if ((e = allow_smem((const void*)pick_fft<double>(l, s, op, pp))) != cudaSuccess) return e;
+                    if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp))) != cudaSuccess) return e;
                 }
-    if ((e = cudaFuncSetAttribute(dense_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(dense_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+    if ((e = allow_smem((const void*)dense_pass_kernel<double>)) != cudaSuccess) return e;
+    if ((e = allow_smem((const void*)dense_pass_kernel<float>)) != cudaSuccess) return e;
     done = true;
     return cudaSuccess;
+}
+
+static int env_flag(const char* name, int dflt) {
+    const char* v = getenv(name);
+    if (!v || !*v) return dflt;
+    return atoi(v);
 }
 
 cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
@@ -258,7 +294,39 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);
     const bool strided = p.family == FAM_STRIDED;
-    const size_t smem = fft_pass_smem_bytes(p, f32 ? 4 : 8);
+    const int rb = f32 ? 4 : 8;
+    // pipelined strided path for long lines (FP_SPIPE=0 disables; FP_SPIPE_MINLOG sets
+    // the shortest line): forward / inverse passes on a typed operand, no DST, not
+    // the first pass, and only when two tiles of the planned width fit (measured:
+    // halving the width or pipelining the fp64-heavy MID step loses)
+    static const int use_spipe = env_flag("FP_SPIPE", 1);
+    static const int spipe_min = env_flag("FP_SPIPE_MINLOG", 9);
+    const bool cin = (p.op == OP_INV) ? (p.ikind == IK_ICFFT || p.ikind == IK_IRFFT) : (p.fkind == FK_CFFT);
+    const int want = cin ? (f32 ? ET_C64 : ET_C128) : (f32 ? ET_F32 : ET_F64);
+    const bool dst = (p.op != OP_INV && p.fkind == FK_DST2) || (p.op != OP_FWD && p.ikind == IK_DST3);
+    const size_t psmem = 2 * linfo_bytes(p.lines) + 2 * (size_t)p.lines * p.ls * 2 * rb;
+    if (use_spipe && strided && p.op != OP_MID && p.logM >= spipe_min && !dst && p.nonfinite == nullptr &&
+        p.g.in_type == want && psmem <= 227 * 1024) {
+        FftKernelFn fn = f32 ? pick_fft<float>(p.logM, true, p.op, true) : pick_fft<double>(p.logM, true, p.op, true);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // ... and only where the regular kernel is held to one CTA per SM (with two
+        // or more resident CTAs their load / compute phases already overlap)
+        FftKernelFn reg = f32 ? pick_fft<float>(p.logM, true, p.op, false) : pick_fft<double>(p.logM, true, p.op, false);
+        int reg_per_sm = 0;
+        if (reg) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&reg_per_sm, (const void*)reg, threads,
+                                                              fft_pass_smem_bytes(p, rb));
+        if (fn && reg_per_sm == 1 &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, threads, psmem) == cudaSuccess &&
+            per_sm > 0) {
+            long long grid = (long long)sms * per_sm;
+            if (grid > p.tiles) grid = p.tiles;
+            fn<<<(int)grid, threads, psmem, st>>>(p);
+            return cudaGetLastError();
+        }
+    }
+    const size_t smem = fft_pass_smem_bytes(p, rb);
     FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false) : pick_fft<double>(p.logM, strided, p.op, false);
     if (!fn) return cudaErrorInvalidValue;
     fn<<<p.tiles, threads, smem, st>>>(p);

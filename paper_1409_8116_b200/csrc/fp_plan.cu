@@ -31,6 +31,7 @@ cudaError_t launch_scale_pass(const ScalePass& p, bool f32, cudaStream_t st);
 cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st);
 cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* out, int out_type, cudaStream_t st);
 size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
+int strided_line_stride(const FftPass& p, bool f32);
 }  // namespace fpb
 
 using namespace fpb;
@@ -269,7 +270,9 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
     int lines;
     // FP_TILE_THREADS_CONTIG / FP_TILE_BYTES_STRIDED: tuning overrides (benchmarks only)
     static const int contig_threads = env_int("FP_TILE_THREADS_CONTIG", 128);
-    static const int strided_bytes = env_int("FP_TILE_BYTES_STRIDED", 128);
+    static const int strided_bytes_io = env_int("FP_TILE_BYTES_STRIDED", 128);
+    static const int strided_bytes_mid = env_int("FP_TILE_BYTES_MID", 64);
+    const int strided_bytes = p.op == OP_MID ? strided_bytes_mid : strided_bytes_io;
     if (p.family == FAM_CONTIG) {
         lines = std::max(1, contig_threads >> logTL);
         const long long nl = na * nb;
@@ -288,9 +291,11 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
         while (lines > 1 && lines / 2 >= nb) lines /= 2;
         p.lines = lines;
         p.logLines = ilog2(lines);
+        p.ls = strided_line_stride(p, f32);
         while (p.lines > 1 && ((p.lines << logTL) > 512 || fft_pass_smem_bytes(p, real_bytes) > 200 * 1024)) {
             p.lines /= 2;
             p.logLines -= 1;
+            p.ls = strided_line_stride(p, f32);
         }
         p.nbt = (int)((nb + p.lines - 1) / p.lines);
         p.tiles = (int)(na * p.nbt);
