@@ -48,20 +48,23 @@ def is_stale() -> bool:
     return any(f.stat().st_mtime > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, extra_flags=(), lib_path=None) -> Path:
     """Compile the library if missing or older than its sources (one nvcc per
-    translation unit, in parallel, then one link)."""
-    if not force and not is_stale():
+    translation unit, in parallel, then one link).  ``extra_flags`` / ``lib_path``
+    build a variant library elsewhere (A/B benchmarks, tools/build_variant.py)."""
+    if lib_path is None and not extra_flags and not force and not is_stale():
         return LIB_PATH
+    lib_out = Path(lib_path) if lib_path is not None else LIB_PATH
+    obj_dir = OBJ_DIR if lib_path is None else lib_out.parent / (lib_out.stem + "_obj")
     from concurrent.futures import ThreadPoolExecutor
 
-    LIB_DIR.mkdir(parents=True, exist_ok=True)
-    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+    lib_out.parent.mkdir(parents=True, exist_ok=True)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     nvcc = nvcc_path()
 
     def compile_one(src):
-        obj = OBJ_DIR / (src + ".o")
-        cmd = [nvcc, *ARCH_FLAGS, *COMPILE_FLAGS, "-c", str(CSRC / src), "-o", str(obj)]
+        obj = obj_dir / (src + ".o")
+        cmd = [nvcc, *ARCH_FLAGS, *COMPILE_FLAGS, *extra_flags, "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         proc = subprocess.run(cmd, capture_output=True, text=True)
@@ -72,15 +75,15 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     workers = max(1, min(len(SOURCES), os.cpu_count() or 1))
     with ThreadPoolExecutor(max_workers=workers) as pool:
         objs = list(pool.map(compile_one, SOURCES))
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    tmp = lib_out.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH_FLAGS, *LINK_FLAGS, "-o", str(tmp), *map(str, objs)]
     if verbose:
         print(" ".join(cmd), flush=True)
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":  # pragma: no cover

@@ -8,6 +8,7 @@ library is loaded lazily; a missing or unloadable library raises immediately
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from ctypes import POINTER, Structure, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p, c_char_p
 
@@ -124,7 +125,8 @@ def load(path=None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = str(path or LIB_PATH)
+        # FP_NATIVE_LIB: a variant build of the same library (A/B benchmarks only)
+        p = str(path or os.environ.get("FP_NATIVE_LIB") or LIB_PATH)
         try:
             lib = ctypes.CDLL(p)
         except OSError as exc:

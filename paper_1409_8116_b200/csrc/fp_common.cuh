@@ -120,6 +120,16 @@ __host__ __device__ constexpr int stage_tw_offset(int logM, int logNs) {
 }
 __host__ __device__ constexpr int stage_tw_total(int logM) { return stage_tw_offset(logM, logM); }
 
+// radix-16 stages form 9 of their 15 twiddles as products of two table
+// entries (per precision; A/B switches for variant builds)
+#ifndef FP_TW2_F32
+#define FP_TW2_F32 1
+#endif
+#ifndef FP_TW2_F64
+#define FP_TW2_F64 1
+#endif
+template <typename T> inline constexpr bool kTwoLevelTwiddles = sizeof(T) == 4 ? FP_TW2_F32 : FP_TW2_F64;
+
 template <int R, int LOGNS, bool INV, typename T, int LOGM, bool FROM_REG = false, bool TO_REG = false>
 __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* __restrict__ W,
                                                cx<T>* vio = nullptr) {
@@ -143,10 +153,24 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* 
         }
         if (LOGNS > 0) {
             const cx<T>* tw = reinterpret_cast<const cx<T>*>(W) + stage_tw_offset(LOGM, LOGNS) + (j & (NS - 1));
+            if constexpr (R == 16 && kTwoLevelTwiddles<T>) {
+                // two-level twiddles: load w^r for r in {1,2,3,4,8,12} and form the
+                // other nine as w^(r&3) * w^(r&12) (6 loads instead of 15)
+                cx<T> w[16];
+                w[1] = __ldg(&tw[NS]); w[2] = __ldg(&tw[2 * NS]); w[3] = __ldg(&tw[3 * NS]);
+                w[4] = __ldg(&tw[4 * NS]); w[8] = __ldg(&tw[8 * NS]); w[12] = __ldg(&tw[12 * NS]);
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                const cx<T> w = __ldg(&tw[r * NS]);
-                v[b * R + r] = INV ? cmulc<T>(v[b * R + r], w) : cmul<T>(v[b * R + r], w);
+                for (int h = 4; h < 16; h += 4)
+#pragma unroll
+                    for (int l = 1; l < 4; ++l) w[h + l] = cmul<T>(w[h], w[l]);
+#pragma unroll
+                for (int r = 1; r < R; ++r) v[b * R + r] = INV ? cmulc<T>(v[b * R + r], w[r]) : cmul<T>(v[b * R + r], w[r]);
+            } else {
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const cx<T> w = __ldg(&tw[r * NS]);
+                    v[b * R + r] = INV ? cmulc<T>(v[b * R + r], w) : cmul<T>(v[b * R + r], w);
+                }
             }
         }
         dft_reg<R, INV, T>(v + b * R);

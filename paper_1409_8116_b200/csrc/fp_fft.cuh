@@ -471,6 +471,31 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     const T* zr_io = reinterpret_cast<const T*>(line_io);
     const LineInfo Lio = linfo[lio];
 
+    if constexpr (OP == OP_MID) {
+        if (p.fkind == FK_CFFT) {
+            // complex lines: the eigenvalue divide is pointwise, so the forward FFT
+            // ends in registers (v[r] = Z[jt + TL r]), is scaled there, and the
+            // inverse FFT starts from them -- two shared-memory round trips fewer
+            const Scaling& Sc = p.s;
+            const LineInfo L = linfo[lf];
+            const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+            const double cst = Sc.bscale * Sc.inv_np;
+            cx<T> v[16];
+            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            if (jt == 0) {
+                if (cap) *Sc.dc_out = (double)v[0].x;
+                v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
+            } else {
+                v[0] = cscale<T>(v[0], eig_factor_nz<T>(Sc, L, jt, cst));
+            }
+#pragma unroll
+            for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
+            fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+            compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
+            return;
+        }
+    }
+
     if constexpr (fwd_in) {
         fft_tile<false, T, LOGM>(line_f, jt, W);
 
