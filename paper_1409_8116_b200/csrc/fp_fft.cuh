@@ -38,11 +38,29 @@ __device__ __forceinline__ int line_stride(const FftPass& p) {
     else return Shape<LOGM>::LS;
 }
 
+// The OP template parameter: the pass op in the low 4 bits; a MID specialised
+// on its line kind carries kind + 1 above them (0 = kind read at run time from
+// FftPass).  One kind per kernel keeps the MID's code small (ncu: c3 MID lost
+// ~9 % of its issue slots to instruction-cache misses with all four kinds).
+__host__ __device__ constexpr int opb(int op) { return op & 15; }
+__host__ __device__ constexpr int opkind(int op) { return (op >> 4) - 1; }
+__host__ __device__ constexpr int mid_op(int kind) { return OP_MID | ((kind + 1) << 4); }
+template <int OP>
+__device__ __forceinline__ int fkind_of(const FftPass& p) {
+    if constexpr (opkind(OP) >= 0) return opkind(OP);
+    else return p.fkind;
+}
+template <int OP>   // forward and inverse kinds of a pair share their enum value
+__device__ __forceinline__ int ikind_of(const FftPass& p) {
+    if constexpr (opkind(OP) >= 0) return opkind(OP);
+    else return p.ikind;
+}
+
 // does this (op, kind) read complex lines?
 template <int OP>
 __device__ __forceinline__ bool complex_input(const FftPass& p) {
-    if (OP == OP_INV) return p.ikind == IK_ICFFT || p.ikind == IK_IRFFT;
-    return p.fkind == FK_CFFT;
+    if (opb(OP) == OP_INV) return ikind_of<OP>(p) == IK_ICFFT || ikind_of<OP>(p) == IK_IRFFT;
+    return fkind_of<OP>(p) == FK_CFFT;
 }
 
 // ----------------------------------------------------------------------------
@@ -74,7 +92,7 @@ __device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo
     L.null_line = (iag == 0 && ibg == 0);
     double before = 0.0, a1 = 0.0, a2 = 0.0;
     int nafter = 0;
-    if (OP == OP_MID) {
+    if (opb(OP) == OP_MID) {
         const bool ha = p.s.lam_a != nullptr, hb = p.s.lam_b != nullptr;
         const double la = (ha && valid) ? p.s.lam_a[iag] : 0.0;
         const double lb = (hb && valid) ? p.s.lam_b[ibg] : 0.0;
@@ -190,7 +208,7 @@ template <typename T, int LOGM, bool STRIDED, int OP>
 __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio, cx<T>* line_io, int bio) {
     using S = Shape<LOGM>;
     constexpr int M = S::M, TL = S::TL;
-    constexpr bool fwd_in = OP != OP_INV;
+    constexpr bool fwd_in = opb(OP) != OP_INV;
     constexpr int n = 2 * M;   // real kinds (unused by the complex ones)
     T* zr_io = reinterpret_cast<T*>(line_io);
     bool bad = false;
@@ -199,8 +217,8 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
     const cx<T>* cline = reinterpret_cast<const cx<T>*>(p.g.in) + Lio.in_off;
     const long long st = p.g.in_st;
     cx<T> v[16];
-    if (fwd_in && p.fkind != FK_CFFT) {
-        const int kind = p.fkind;
+    if (fwd_in && fkind_of<OP>(p) != FK_CFFT) {
+        const int kind = fkind_of<OP>(p);
         if (!STRIDED) {
             load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
             if (chk) {
@@ -259,7 +277,7 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
         }
     } else {
         // DCT-III / DST-III: real spectrum of n = 2M entries
-        const bool dst = p.ikind == IK_DST3;
+        const bool dst = ikind_of<OP>(p) == IK_DST3;
         if (!STRIDED) {
             load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
             if (chk) {
@@ -305,7 +323,7 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
 template <typename T, int LOGM, int OP>
 __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& Lio, cx<T>* line_io, int bio) {
     constexpr int M = 1 << LOGM;
-    if (OP != OP_INV || p.ikind != IK_IRFFT || bio != 0) return false;
+    if (opb(OP) != OP_INV || ikind_of<OP>(p) != IK_IRFFT || bio != 0) return false;
     cx<T> xm = mkc<T>(0, 0);
     if (Lio.valid) xm = __ldg(reinterpret_cast<const cx<T>*>(p.g.in) + Lio.in_off + (long long)M * p.g.in_st);
     line_io[P(M)] = xm;
@@ -313,7 +331,7 @@ __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& 
 }
 
 // store of an inverse-transformed tile (natural-order data in shared memory)
-template <typename T, int LOGM, bool STRIDED>
+template <typename T, int LOGM, bool STRIDED, int OP>
 __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
@@ -328,7 +346,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
     const T* zr_io = reinterpret_cast<const T*>(line_io);
     const LineInfo Lio = linfo[lio];
         if (!Lio.valid) return;
-        const int ik = p.ikind;
+        const int ik = ikind_of<OP>(p);
         const T om = (T)p.out_mult;
         const long long ob = Lio.out_off;
         const long long os = g.out_st;
@@ -454,7 +472,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF;
     const int LS = line_stride<T, LOGM, STRIDED>(p);
-    constexpr bool fwd_in = OP != OP_INV;
+    constexpr bool fwd_in = opb(OP) != OP_INV;
     const int tid = threadIdx.x;
     const int Lc = p.lines, logL = p.logLines;
     constexpr int n = 2 * M;   // real kinds (unused by the complex ones)
@@ -471,8 +489,8 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     const T* zr_io = reinterpret_cast<const T*>(line_io);
     const LineInfo Lio = linfo[lio];
 
-    if constexpr (OP == OP_MID) {
-        if (p.fkind == FK_CFFT) {
+    if constexpr (opb(OP) == OP_MID) {
+        if (fkind_of<OP>(p) == FK_CFFT) {
             // complex lines: the eigenvalue divide is pointwise, so the forward FFT
             // ends in registers (v[r] = Z[jt + TL r]), is scaled there, and the
             // inverse FFT starts from them -- two shared-memory round trips fewer
@@ -491,7 +509,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
 #pragma unroll
             for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
             fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
-            compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
+            compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
             return;
         }
     }
@@ -499,8 +517,8 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     if constexpr (fwd_in) {
         fft_tile<false, T, LOGM>(line_f, jt, W);
 
-        if constexpr (OP == OP_FWD) {
-            const int kind = p.fkind;
+        if constexpr (opb(OP) == OP_FWD) {
+            const int kind = fkind_of<OP>(p);
             const T om = (T)p.out_mult;
             if constexpr (STRIDED) {
                 // thread (column, block b) owns quads q = 8 b + i, i < 8 (CFFT: k = 16 b + i):
@@ -648,7 +666,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             return;
         } else {
             // ---- OP_MID: post -> capture -> scale -> pre, in place on each quad/pair
-            const int kind = p.fkind;
+            const int kind = fkind_of<OP>(p);
             const Scaling& Sc = p.s;
             const LineInfo L = linfo[lf];
             const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
@@ -739,7 +757,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
         }
     } else {
         // =============== INVERSE pre-processing (line-major mapping)
-        const int ik = p.ikind;
+        const int ik = ikind_of<OP>(p);
         if (ik == IK_DCT3 || ik == IK_DST3) {
             // two-phase: the real-valued view overlaps the complex slots
             const T* zr = reinterpret_cast<const T*>(line_f);
@@ -796,10 +814,10 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
         }
     }
 
-    if constexpr (OP != OP_FWD) {
+    if constexpr (opb(OP) != OP_FWD) {
         // =============== INVERSE FFT + store (INV and MID)
         fft_tile<true, T, LOGM>(line_f, jt, W);
-        compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
+        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
     }
 }
 
@@ -857,11 +875,11 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
     cx<T>* line_f = sm + lf * LS;
     cx<T> v[16], pz[8];
 
-    if constexpr (OP == OP_FWD) {
+    if constexpr (opb(OP) == OP_FWD) {
         // CONTIG only: I/O mapping == line-major mapping
         fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
         const LineInfo L = linfo[lf];
-        const int kind = p.fkind;
+        const int kind = fkind_of<OP>(p);
         const T om = (T)p.out_mult;
         if (kind == FK_CFFT) {
             if (!L.valid) return;
@@ -920,9 +938,9 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         }
         return;
     } else {
-        if constexpr (OP == OP_MID) {
+        if constexpr (opb(OP) == OP_MID) {
             fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
-            const int kind = p.fkind;
+            const int kind = fkind_of<OP>(p);
             const Scaling& Sc = p.s;
             const LineInfo L = linfo[lf];
             const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
@@ -1006,7 +1024,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
             }
         } else {
             // OP_INV, real kinds: pre-processing from the placed spectrum
-            const int ik = p.ikind;
+            const int ik = ikind_of<OP>(p);
             cx<T> half0 = mkc<T>(0, 0);
             if (ik == IK_IRFFT) {
 #pragma unroll
@@ -1051,7 +1069,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         // inverse FFT from registers (its first write is preceded by a barrier,
         // so the pre-processing reads above are complete)
         fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
-        compute_store_tail<T, LOGM, STRIDED>(p, linfo, sm);
+        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
     }
 }
 
@@ -1074,8 +1092,8 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     bad |= place_nyquist<T, LOGM, OP>(p, Lio, line_io, bio);
     if (bad) *p.nonfinite = 1;
     __syncthreads();
-    if constexpr (S::TL <= 32 && !(OP == OP_FWD && STRIDED)) {
-        if (OP != OP_INV || p.ikind != IK_ICFFT) {
+    if constexpr (S::TL <= 32 && !(opb(OP) == OP_FWD && STRIDED)) {
+        if (opb(OP) != OP_INV || ikind_of<OP>(p) != IK_ICFFT) {
             compute_store_reg<T, LOGM, STRIDED, OP>(p, linfo, sm);
             return;
         }
@@ -1129,15 +1147,15 @@ __device__ __forceinline__ void issue_tile_async(const FftPass& p, const LineInf
 #pragma unroll
         for (int it = 0; it < 16; ++it)
             cp_async_elem<sizeof(cx<T>)>(line + 17 * b + it, src + row_off(16 * b + it));
-        if (OP == OP_INV && p.ikind == IK_IRFFT && b == 0)
+        if (opb(OP) == OP_INV && ikind_of<OP>(p) == IK_IRFFT && b == 0)
             cp_async_elem<sizeof(cx<T>)>(line + P(M), src + (long long)M * st);
     } else {
         const T* src = reinterpret_cast<const T*>(g.in) + L.in_off;
         const RowBlk rb(b, n);
-        if (OP == OP_INV) {             // DCT-III: real spectrum in the PR layout
+        if (opb(OP) == OP_INV) {             // DCT-III: real spectrum in the PR layout
 #pragma unroll
             for (int it = 0; it < 32; ++it) cp_async_elem<sizeof(T)>(zr + rb.pr + it, src + (long long)(32 * b + it) * st);
-        } else if (p.fkind == FK_RFFT) {
+        } else if (fkind_of<OP>(p) == FK_RFFT) {
 #pragma unroll
             for (int it = 0; it < 32; ++it) cp_async_elem<sizeof(T)>(zr + rb.r34 + it, src + row_off(32 * b + it));
         } else {                        // DCT-II: Makhoul reordering
@@ -1172,8 +1190,8 @@ __global__ void __launch_bounds__(512) fft_pass_spipe(const FftPass p) {
         cp_async_commit_group();
         cp_async_wait_prev();  // this thread's copies of `tile` have landed
         __syncthreads();       // ... and everybody's
-        if constexpr (S::TL <= 32 && OP != OP_FWD) {
-            if (OP != OP_INV || p.ikind != IK_ICFFT) {
+        if constexpr (S::TL <= 32 && opb(OP) != OP_FWD) {
+            if (opb(OP) != OP_INV || ikind_of<OP>(p) != IK_ICFFT) {
                 compute_store_reg<T, LOGM, true, OP>(p, lc, zc);
                 continue;
             }
@@ -1184,7 +1202,7 @@ __global__ void __launch_bounds__(512) fft_pass_spipe(const FftPass p) {
 
 template <typename T, int L, int OPV>
 inline FftKernelFn spipe_fn(bool strided) {
-    if constexpr (OPV == OP_MID) return nullptr;   // the MID step is not pipelined
+    if constexpr (opb(OPV) == OP_MID) return nullptr;   // the MID step is not pipelined
     else return strided ? (FftKernelFn)fft_pass_spipe<T, L, OPV> : (FftKernelFn) nullptr;
 }
 
@@ -1201,13 +1219,26 @@ inline FftKernelFn spipe_fn(bool strided) {
         if (pipe) return FP_FFT_PIPE_FN(T, L, s, OPV);                                                \
         return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_kernel<T, L, false, OPV>;              \
     }                                                                                                 \
-    template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op, bool pipe) {             \
-        if constexpr (L > HI) { return nullptr; }                                                     \
-        else {                                                                                        \
-            if (logM != L) return NAME##_rec<L + 1>(logM, s, op, pipe);                               \
-            return op == OP_FWD ? NAME##_one<L, OP_FWD>(s, pipe)                                      \
-                 : op == OP_INV ? NAME##_one<L, OP_INV>(s, pipe) : NAME##_one<L, OP_MID>(s, pipe);    \
+    template <int L> static FftKernelFn NAME##_mid(bool s, bool pipe, int kind) {                     \
+        if (pipe || !s || kind < 0) return NAME##_one<L, OP_MID>(s, pipe);                            \
+        switch (kind) {                                                                               \
+            case FK_DCT2: return fft_pass_kernel<T, L, true, mid_op(FK_DCT2)>;                        \
+            case FK_DST2: return fft_pass_kernel<T, L, true, mid_op(FK_DST2)>;                        \
+            case FK_RFFT: return fft_pass_kernel<T, L, true, mid_op(FK_RFFT)>;                        \
+            default: /* fp64 complex: the specialised build spills (c4 MID +7 %) */                  \
+                if constexpr (sizeof(T) == 8) return NAME##_one<L, OP_MID>(s, pipe);                  \
+                else return fft_pass_kernel<T, L, true, mid_op(FK_CFFT)>;                             \
         }                                                                                             \
     }                                                                                                 \
-    FftKernelFn NAME(int logM, bool s, int op, bool pipe) { return NAME##_rec<LO>(logM, s, op, pipe); } \
+    template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op, bool pipe, int kind) {   \
+        if constexpr (L > HI) { return nullptr; }                                                     \
+        else {                                                                                        \
+            if (logM != L) return NAME##_rec<L + 1>(logM, s, op, pipe, kind);                         \
+            return op == OP_FWD ? NAME##_one<L, OP_FWD>(s, pipe)                                      \
+                 : op == OP_INV ? NAME##_one<L, OP_INV>(s, pipe) : NAME##_mid<L>(s, pipe, kind);      \
+        }                                                                                             \
+    }                                                                                                 \
+    FftKernelFn NAME(int logM, bool s, int op, bool pipe, int kind) {                                 \
+        return NAME##_rec<LO>(logM, s, op, pipe, kind);                                               \
+    }                                                                                                 \
     }

@@ -34,10 +34,10 @@
 namespace fpb {
 
 using FftKernelFn = void (*)(const FftPass);
-FftKernelFn pick_fft_d_lo(int logM, bool strided, int op, bool pipe);
-FftKernelFn pick_fft_d_hi(int logM, bool strided, int op, bool pipe);
-FftKernelFn pick_fft_f_lo(int logM, bool strided, int op, bool pipe);
-FftKernelFn pick_fft_f_hi(int logM, bool strided, int op, bool pipe);
+FftKernelFn pick_fft_d_lo(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_hi(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_lo(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_hi(int logM, bool strided, int op, bool pipe, int kind);
 
 // ----------------------------------------------------------------------------
 // dense engine: out_k = sum_j mat[k][j] * in_j, one tile of lines per CTA
@@ -249,9 +249,11 @@ size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes) {
 }
 
 template <typename T>
-static FftKernelFn pick_fft(int logM, bool strided, int op, bool pipe) {
-    if (sizeof(T) == 8) return logM <= 8 ? pick_fft_d_lo(logM, strided, op, pipe) : pick_fft_d_hi(logM, strided, op, pipe);
-    return logM <= 8 ? pick_fft_f_lo(logM, strided, op, pipe) : pick_fft_f_hi(logM, strided, op, pipe);
+static FftKernelFn pick_fft(int logM, bool strided, int op, bool pipe, int kind = -1) {
+    // kind >= 0 selects the MID specialised on that line kind (strided, non-pipelined)
+    if (sizeof(T) == 8)
+        return logM <= 8 ? pick_fft_d_lo(logM, strided, op, pipe, kind) : pick_fft_d_hi(logM, strided, op, pipe, kind);
+    return logM <= 8 ? pick_fft_f_lo(logM, strided, op, pipe, kind) : pick_fft_f_hi(logM, strided, op, pipe, kind);
 }
 
 // Opt in to the full 227 KB per CTA AND ask for the max-shared carveout: left to
@@ -274,8 +276,10 @@ static cudaError_t set_smem_attr() {
         for (int s = 0; s < 2; ++s)
             for (int op = 0; op < 3; ++op)
                 for (int pp = 0; pp < 2; ++pp) {
-                    if ((e = allow_smem((const void*)pick_fft<double>(l, s, op, pp))) != cudaSuccess) return e;
-                    if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp))) != cudaSuccess) return e;
+                    for (int kind = -1; kind < (op == OP_MID ? 4 : 0); ++kind) {
+                        if ((e = allow_smem((const void*)pick_fft<double>(l, s, op, pp, kind))) != cudaSuccess) return e;
+                        if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp, kind))) != cudaSuccess) return e;
+                    }
                 }
     if ((e = allow_smem((const void*)dense_pass_kernel<double>)) != cudaSuccess) return e;
     if ((e = allow_smem((const void*)dense_pass_kernel<float>)) != cudaSuccess) return e;
@@ -327,7 +331,10 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
         }
     }
     const size_t smem = fft_pass_smem_bytes(p, rb);
-    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false) : pick_fft<double>(p.logM, strided, p.op, false);
+    static const int mid_spec = env_flag("FP_MID_KIND_KERNELS", 1);   // 0: one MID kernel for all kinds (A/B)
+    const int kind = (p.op == OP_MID && mid_spec) ? p.fkind : -1;
+    FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false, kind)
+                         : pick_fft<double>(p.logM, strided, p.op, false, kind);
     if (!fn) return cudaErrorInvalidValue;
     fn<<<p.tiles, threads, smem, st>>>(p);
     return cudaGetLastError();
