@@ -1076,7 +1076,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
 // ----------------------------------------------------------------------------
 // general path: one tile per CTA, loads straight from HBM
 template <typename T, int LOGM, bool STRIDED, int OP>
-__global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
+__device__ __forceinline__ void fft_pass_tile(const FftPass& p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using S = Shape<LOGM>;
     LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
@@ -1099,6 +1099,26 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
         }
     }
     compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);
+}
+
+// Strided tiles: up to 512 threads, 128 registers (capping them spills the MID).
+template <typename T, int LOGM, bool STRIDED, int OP>
+__global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
+    fft_pass_tile<T, LOGM, STRIDED, OP>(p);
+}
+
+// Contiguous tiles trade registers for residency: capped at 72 (fp32) / 96 (fp64)
+// they run 5-7 CTAs/SM instead of 4 (c5 line passes 16.5 -> 14.4 ms; c3 -2 %).
+#ifndef FP_CONTIG_REGS_F32
+#define FP_CONTIG_REGS_F32 72
+#endif
+#ifndef FP_CONTIG_REGS_F64
+#define FP_CONTIG_REGS_F64 96
+#endif
+template <typename T> struct ContigRegs { static constexpr int v = sizeof(T) == 4 ? FP_CONTIG_REGS_F32 : FP_CONTIG_REGS_F64; };
+template <typename T, int LOGM, int OP>
+__global__ void __maxnreg__(ContigRegs<T>::v) fft_pass_contig(const FftPass p) {
+    fft_pass_tile<T, LOGM, false, OP>(p);
 }
 
 // ----------------------------------------------------------------------------
@@ -1217,7 +1237,7 @@ inline FftKernelFn spipe_fn(bool strided) {
     namespace fpb {                                                                                   \
     template <int L, int OPV> static FftKernelFn NAME##_one(bool s, bool pipe) {                      \
         if (pipe) return FP_FFT_PIPE_FN(T, L, s, OPV);                                                \
-        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_kernel<T, L, false, OPV>;              \
+        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_contig<T, L, OPV>;                     \
     }                                                                                                 \
     template <int L> static FftKernelFn NAME##_mid(bool s, bool pipe, int kind) {                     \
         if (pipe || !s || kind < 0) return NAME##_one<L, OP_MID>(s, pipe);                            \
