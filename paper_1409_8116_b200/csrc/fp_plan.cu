@@ -269,7 +269,7 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
     const int real_bytes = f32 ? 4 : 8;
     int lines;
     // FP_TILE_THREADS_CONTIG / FP_TILE_BYTES_STRIDED: tuning overrides (benchmarks only)
-    static const int contig_threads = env_int("FP_TILE_THREADS_CONTIG", 128);
+    static const int contig_threads = env_int("FP_TILE_THREADS_CONTIG", 32);
     static const int strided_bytes_io = env_int("FP_TILE_BYTES_STRIDED", 128);
     static const int strided_bytes_mid = env_int("FP_TILE_BYTES_MID", 64);
     const int strided_bytes = p.op == OP_MID ? strided_bytes_mid : strided_bytes_io;
