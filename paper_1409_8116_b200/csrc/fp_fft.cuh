@@ -200,6 +200,63 @@ struct RowBlk {
     __device__ __forceinline__ int makhoul(int i) const { return (i & 1) ? (mk_o - (i >> 1)) : (mk_e + (i >> 1)); }
 };
 
+// 2 V_k of the real-FFT untangle (same as rsplit2 below; needed earlier in the file)
+template <typename T>
+__device__ __forceinline__ cx<T> rsplit2_fwd(cx<T> zk, cx<T> zm, cx<T> tk) {
+    const cx<T> A = mkc<T>(zk.x + zm.x, zk.y - zm.y);
+    const cx<T> B = mkc<T>(zk.x - zm.x, zk.y + zm.y);
+    const cx<T> tB = cmul<T>(tk, B);
+    return mkc<T>(A.x + tB.y, A.y - tB.x);
+}
+// ----------------------------------------------------------------------------
+// DCT-I / DST-I as a real FFT of length 2M (identities checked against scipy in
+// oracle.r1_via_rfft): with z the even extension of x (DCT-I, n = M + 1,
+// z_j = x_j for j <= M, x_{2M-j} above) or the odd one (DST-I, n = M - 1, z_0 =
+// z_M = 0, z_j = x_{j-1} below M, -x_{2M-j-1} above) and V = rFFT_2M(z):
+//   DCT-I X_k = Re V_k (k = 0..M),  DST-I X_{k-1} = -Im V_k (k = 1..M-1);
+// the inverse of either is the unnormalised inverse real FFT of the half
+// spectrum (X_k, 0) resp. (0, -X_{k-1}), truncated to the n outputs.
+template <int OP>
+__device__ __forceinline__ bool is_r1(const FftPass& p) {
+    return (opb(OP) == OP_INV ? ikind_of<OP>(p) : fkind_of<OP>(p)) >= FK_DCT1;
+}
+// index of x feeding z_j (always a valid index) and the factor (0, 1 or -1) it enters with
+template <int M>
+__device__ __forceinline__ int r1_src(bool d1, int j, int* sgn) {
+    if (d1) { *sgn = 1; return j <= M ? j : 2 * M - j; }
+    if (j == 0 || j == M) { *sgn = 0; return 0; }
+    if (j < M) { *sgn = 1; return j - 1; }
+    *sgn = -1;
+    return 2 * M - j - 1;
+}
+template <typename T>
+__device__ __forceinline__ T r1_apply(T v, int sgn) { return sgn == 0 ? (T)0 : (sgn < 0 ? -v : v); }
+
+// forward outputs of the pair (q, M - q), 0 < q < M/2, from the tile values zk = Z_q, zm = Z_{M-q}
+template <typename T, int M>
+__device__ __forceinline__ void r1_store_pair(T* pb, long long os, bool d1, int q, cx<T> zk, cx<T> zm, cx<T> tq, T omh) {
+    const cx<T> Vq = rsplit2_fwd<T>(zk, zm, tq), Vm = rsplit2_fwd<T>(zm, zk, t_mirror<T>(tq));
+    if (d1) {
+        pb[(long long)q * os] = Vq.x * omh;
+        pb[(long long)(M - q) * os] = Vm.x * omh;
+    } else {
+        pb[(long long)(q - 1) * os] = -Vq.y * omh;
+        pb[(long long)(M - q - 1) * os] = -Vm.y * omh;
+    }
+}
+// ... and of the self-paired entries k = 0, M (from Z_0) and M/2
+template <typename T, int M>
+__device__ __forceinline__ void r1_store_dc(T* pb, long long os, bool d1, cx<T> z0, cx<T> zh, cx<T> th, T om, T omh) {
+    const cx<T> Vh = rsplit2_fwd<T>(zh, zh, th);
+    if (d1) {
+        pb[0] = (z0.x + z0.y) * om;
+        pb[(long long)M * os] = (z0.x - z0.y) * om;
+        pb[(long long)(M / 2) * os] = Vh.x * omh;
+    } else {
+        pb[(long long)(M / 2 - 1) * os] = -Vh.y * omh;
+    }
+}
+
 // ----------------------------------------------------------------------------
 // placement: line values -> padded complex tile in the layout the FFT expects
 // (Makhoul reordering / half-length packing for real kinds).  Returns the
@@ -217,6 +274,69 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
     const cx<T>* cline = reinterpret_cast<const cx<T>*>(p.g.in) + Lio.in_off;
     const long long st = p.g.in_st;
     cx<T> v[16];
+    if (is_r1<OP>(p)) {
+        const bool d1 = (fwd_in ? fkind_of<OP>(p) : ikind_of<OP>(p)) == FK_DCT1;
+        if constexpr (fwd_in) {
+            // the extension z (2M reals) in the half-FFT packing
+            T z[32];
+            int sg[32];
+            if (!STRIDED) {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) {
+                    const int j0 = 2 * (bio + it * TL);
+                    const int i0 = r1_src<M>(d1, j0, &sg[2 * it]), i1 = r1_src<M>(d1, j0 + 1, &sg[2 * it + 1]);
+                    z[2 * it] = Lio.valid ? __ldg(rline + (long long)i0 * st) : (T)0;
+                    z[2 * it + 1] = Lio.valid ? __ldg(rline + (long long)i1 * st) : (T)0;
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < 32; ++it) {
+                    const int i0 = r1_src<M>(d1, 32 * bio + it, &sg[it]);
+                    z[it] = Lio.valid ? __ldg(rline + (long long)i0 * st) : (T)0;
+                }
+            }
+            if (chk) {
+#pragma unroll
+                for (int it = 0; it < 32; ++it) bad |= !finite_t(z[it]);
+            }
+#pragma unroll
+            for (int it = 0; it < 32; ++it) z[it] = r1_apply<T>(z[it], sg[it]);
+            if (!STRIDED) {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) line_io[P(bio + it * TL)] = mkc<T>(z[2 * it], z[2 * it + 1]);
+            } else {
+                const RowBlk rb(bio, n);
+#pragma unroll
+                for (int it = 0; it < 32; ++it) zr_io[rb.r34 + it] = z[it];
+            }
+        } else {
+            // the half spectrum (X_k, 0) (DCT-I) or (0, -X_{k-1}) (DST-I), k = 0..M
+            T x[16];
+            int kk[16];
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                kk[it] = STRIDED ? 16 * bio + it : bio + it * TL;
+                const int src = d1 ? kk[it] : (kk[it] == 0 ? 0 : kk[it] - 1);
+                x[it] = Lio.valid ? __ldg(rline + (long long)src * st) : (T)0;
+            }
+            if (chk) {
+#pragma unroll
+                for (int it = 0; it < 16; ++it) bad |= !finite_t(x[it]);
+            }
+#pragma unroll
+            for (int it = 0; it < 16; ++it) {
+                const cx<T> s = d1 ? mkc<T>(x[it], 0) : mkc<T>(0, kk[it] == 0 ? (T)0 : -x[it]);
+                if (STRIDED) line_io[17 * bio + it] = s;
+                else line_io[P(kk[it])] = s;
+            }
+            if (bio == 0) {   // k = M: X_M (DCT-I; n = M + 1) or 0 (DST-I)
+                T xm = (d1 && Lio.valid) ? __ldg(rline + (long long)M * st) : (T)0;
+                if (chk) bad |= !finite_t(xm);
+                line_io[P(M)] = mkc<T>(xm, 0);
+            }
+        }
+        return bad && Lio.valid;
+    }
     if (fwd_in && fkind_of<OP>(p) != FK_CFFT) {
         const int kind = fkind_of<OP>(p);
         if (!STRIDED) {
@@ -362,7 +482,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                     pb[(long long)(k >> lg) * hi + (long long)(k & msk) * os] = cscale<T>(line_io[P(k)], om);
                 }
             } else {
-                const bool dct = ik != IK_IRFFT;
+                const bool dct = ik == IK_DCT3 || ik == IK_DST3;
                 const bool dst = ik == IK_DST3;
                 T* pb = reinterpret_cast<T*>(g.out) + ob;
 #pragma unroll
@@ -388,7 +508,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                 for (int it = 0; it < 16; ++it, po += step) *po = cscale<T>(line_io[P(bio + it * TL)], om);
             }
         } else {
-            const bool dct = ik != IK_IRFFT;
+            const bool dct = ik == IK_DCT3 || ik == IK_DST3;
             const bool dst = ik == IK_DST3;
             T* const pb = reinterpret_cast<T*>(g.out) + ob;
             if (!STRIDED) {
@@ -410,7 +530,15 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                         xv[2 * it + 1] = v.y * om;
                     }
                 }
-                if (p.vec_out) {
+                if (ik >= IK_DCT1) {
+                    // DCT-I keeps z_0..z_M, DST-I z_1..z_{M-1} (shifted down by one)
+                    const bool d1 = ik == IK_DCT1;
+#pragma unroll
+                    for (int it = 0; it < 32; ++it) {
+                        const int j = 2 * (bio + (it >> 1) * TL) + (it & 1);
+                        if (d1 ? (j <= M) : (j >= 1 && j < M)) pb[(long long)(d1 ? j : j - 1) * os] = xv[it];
+                    }
+                } else if (p.vec_out) {
                     cx<T>* po = reinterpret_cast<cx<T>*>(pb) + bio;
 #pragma unroll
                     for (int it = 0; it < 16; ++it) po[it * TL] = mkc<T>(xv[2 * it], xv[2 * it + 1]);
@@ -427,6 +555,14 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                     const T sgn = dst ? -om : om;   // DST-III: odd outputs negated
 #pragma unroll
                     for (int it = 0; it < 32; ++it, po += os) *po = zr_io[rb.makhoul(it)] * ((it & 1) ? sgn : om);
+                } else if (ik >= IK_DCT1) {
+                    const bool d1 = ik == IK_DCT1;
+#pragma unroll
+                    for (int it = 0; it < 32; ++it) {
+                        const int j = 32 * bio + it;
+                        if (d1 ? (j <= M) : (j >= 1 && j < M))
+                            pb[(long long)(d1 ? j : j - 1) * os] = zr_io[rb.r34 + it] * om;
+                    }
                 } else {
 #pragma unroll
                     for (int it = 0; it < 32; ++it, po += os) *po = zr_io[rb.r34 + it] * om;
@@ -556,6 +692,18 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                                 *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
                             }
                         }
+                    } else if (kind >= FK_DCT1) {
+                        const bool d1 = kind == FK_DCT1;
+                        T* const pb = reinterpret_cast<T*>(g.out) + ob;
+                        const T omh = om * (T)0.5;
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            const int q = 8 * b + it;
+                            if (it == 0 && b == 0)
+                                r1_store_dc<T, M>(pb, os, d1, line_io[P(0)], line_io[P(HALF)], Wt[HALF], om, omh);
+                            else
+                                r1_store_pair<T, M>(pb, os, d1, q, line_io[pq0 + it], line_io[PM(it)], Wt[q], omh);
+                        }
                     } else {
                         const bool dst = kind == FK_DST2;
                         T* const pb = reinterpret_cast<T*>(g.out) + ob;
@@ -625,6 +773,18 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                     pq += step; pm -= step;
 #pragma unroll
                     for (int it = 1; it < 8; ++it, pq += step, pm -= step) pair(bio + it * TL);
+                } else if (kind >= FK_DCT1) {
+                    const bool d1 = kind == FK_DCT1;
+                    T* const pb = reinterpret_cast<T*>(g.out) + ob;
+                    const T omh = om * (T)0.5;
+#pragma unroll
+                    for (int it = 0; it < 8; ++it) {
+                        const int q = bio + it * TL;
+                        if (it == 0 && bio == 0)
+                            r1_store_dc<T, M>(pb, os, d1, line_io[P(0)], line_io[P(HALF)], Wt[HALF], om, omh);
+                        else
+                            r1_store_pair<T, M>(pb, os, d1, q, line_io[P(q)], line_io[P(M - q)], Wt[q], omh);
+                    }
                 } else {
                     // DCT-II quads {q, n-q, M-q, M+q} (DST-II: mirrored indices)
                     const bool dst = kind == FK_DST2;
@@ -684,25 +844,34 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                     const int k = jt + it * TL;
                     line_f[P(k)] = cscale<T>(line_f[P(k)], eig_factor_nz<T>(Sc, L, k, cst));
                 }
-            } else if (kind == FK_RFFT) {
+            } else if (kind == FK_RFFT || kind >= FK_DCT1) {
                 const double csth = cst * 0.5;   // the untangle's 1/2
+                // DCT-I keeps the real part of the spectrum, DST-I the imaginary one (the
+                // other vanishes for the extended line; its eigenvalue index is k - 1,
+                // which the planner folds into lam_t)
+                const int r1 = kind == FK_DCT1 ? 1 : (kind == FK_DST1 ? 2 : 0);
+                auto proj = [&](cx<T> x) { return r1 == 1 ? mkc<T>(x.x, 0) : (r1 == 2 ? mkc<T>(0, x.y) : x); };
                 auto pair = [&](int q) {
                     const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
                     const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                    const cx<T> xk = cscale<T>(rsplit2<T>(zk, zm, tq), eig_factor_nz<T>(Sc, L, q, csth));
-                    const cx<T> xm = cscale<T>(rsplit2<T>(zm, zk, tm), eig_factor_nz<T>(Sc, L, M - q, csth));
+                    const cx<T> xk = cscale<T>(proj(rsplit2<T>(zk, zm, tq)), eig_factor_nz<T>(Sc, L, q, csth));
+                    const cx<T> xm = cscale<T>(proj(rsplit2<T>(zm, zk, tm)), eig_factor_nz<T>(Sc, L, M - q, csth));
                     line_f[P(q)] = rmerge<T>(xk, xm, tq);
                     line_f[P(M - q)] = rmerge<T>(xm, xk, tm);
                 };
                 if (jt == 0) {
                     const cx<T> z0 = line_f[P(0)];
-                    T x0 = z0.x + z0.y, xM = z0.x - z0.y;
-                    if (cap) *Sc.dc_out = (double)x0;
-                    x0 *= eig_factor<T>(Sc, L, 0);
-                    xM *= eig_factor<T>(Sc, L, M);
-                    line_f[P(0)] = mkc<T>(x0 + xM, x0 - xM);
+                    if (r1 == 2) {
+                        line_f[P(0)] = mkc<T>(0, 0);   // DST-I: V_0 = V_M = 0
+                    } else {
+                        T x0 = z0.x + z0.y, xM = z0.x - z0.y;
+                        if (cap) *Sc.dc_out = (double)x0;
+                        x0 *= eig_factor<T>(Sc, L, 0);
+                        xM *= eig_factor<T>(Sc, L, M);
+                        line_f[P(0)] = mkc<T>(x0 + xM, x0 - xM);
+                    }
                     const cx<T> zh = line_f[P(HALF)];
-                    const cx<T> xh = cscale<T>(rsplit<T>(zh, zh, Wt[HALF]), eig_factor<T>(Sc, L, HALF));
+                    const cx<T> xh = cscale<T>(proj(rsplit<T>(zh, zh, Wt[HALF])), eig_factor<T>(Sc, L, HALF));
                     line_f[P(HALF)] = rmerge<T>(xh, xh, Wt[HALF]);
                 } else {
                     pair(jt);
@@ -793,7 +962,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                 line_f[P(M - q)] = hold[2 * it + 1];
             }
             __syncthreads();
-        } else if (ik == IK_IRFFT) {
+        } else if (ik == IK_IRFFT || ik >= IK_DCT1) {   // DCT-I / DST-I: placed as a half spectrum
             auto pair = [&](int q) {
                 const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
                 const cx<T> tq = Wt[q];
@@ -1093,12 +1262,12 @@ __device__ __forceinline__ void fft_pass_tile(const FftPass& p) {
     if (bad) *p.nonfinite = 1;
     __syncthreads();
     if constexpr (S::TL <= 32 && !(opb(OP) == OP_FWD && STRIDED)) {
-        if (opb(OP) != OP_INV || ikind_of<OP>(p) != IK_ICFFT) {
+        if ((opb(OP) != OP_INV || ikind_of<OP>(p) != IK_ICFFT) && !is_r1<OP>(p)) {
             compute_store_reg<T, LOGM, STRIDED, OP>(p, linfo, sm);
             return;
         }
     }
-    compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);
+    compute_store<T, LOGM, STRIDED, OP>(p, linfo, sm);   // (DCT-I / DST-I always take this path)
 }
 
 // Strided tiles: up to 512 threads, 128 registers (capping them spills the MID).
@@ -1245,6 +1414,8 @@ inline FftKernelFn spipe_fn(bool strided) {
             case FK_DCT2: return fft_pass_kernel<T, L, true, mid_op(FK_DCT2)>;                        \
             case FK_DST2: return fft_pass_kernel<T, L, true, mid_op(FK_DST2)>;                        \
             case FK_RFFT: return fft_pass_kernel<T, L, true, mid_op(FK_RFFT)>;                        \
+            case FK_DCT1: return fft_pass_kernel<T, L, true, mid_op(FK_DCT1)>;                        \
+            case FK_DST1: return fft_pass_kernel<T, L, true, mid_op(FK_DST1)>;                        \
             default: /* fp64 complex: the specialised build spills (c4 MID +7 %) */                  \
                 if constexpr (sizeof(T) == 8) return NAME##_one<L, OP_MID>(s, pipe);                  \
                 else return fft_pass_kernel<T, L, true, mid_op(FK_CFFT)>;                             \

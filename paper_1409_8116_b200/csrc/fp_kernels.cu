@@ -276,7 +276,7 @@ static cudaError_t set_smem_attr() {
         for (int s = 0; s < 2; ++s)
             for (int op = 0; op < 3; ++op)
                 for (int pp = 0; pp < 2; ++pp) {
-                    for (int kind = -1; kind < (op == OP_MID ? 4 : 0); ++kind) {
+                    for (int kind = -1; kind < (op == OP_MID ? 6 : 0); ++kind) {
                         if ((e = allow_smem((const void*)pick_fft<double>(l, s, op, pp, kind))) != cudaSuccess) return e;
                         if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp, kind))) != cudaSuccess) return e;
                     }
@@ -309,7 +309,8 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     const int want = cin ? (f32 ? ET_C64 : ET_C128) : (f32 ? ET_F32 : ET_F64);
     const bool dst = (p.op != OP_INV && p.fkind == FK_DST2) || (p.op != OP_FWD && p.ikind == IK_DST3);
     const size_t psmem = 2 * linfo_bytes(p.lines) + 2 * (size_t)p.lines * p.ls * 2 * rb;
-    if (use_spipe && strided && p.op != OP_MID && p.logM >= spipe_min && !dst && p.nonfinite == nullptr &&
+    const bool r1 = (p.op == OP_INV ? p.ikind : p.fkind) >= FK_DCT1;   // DCT-I / DST-I: own placement
+    if (use_spipe && strided && p.op != OP_MID && p.logM >= spipe_min && !dst && !r1 && p.nonfinite == nullptr &&
         p.g.in_type == want && psmem <= 227 * 1024) {
         FftKernelFn fn = f32 ? pick_fft<float>(p.logM, true, p.op, true) : pick_fft<double>(p.logM, true, p.op, true);
         int dev = 0, sms = 0, per_sm = 0;

@@ -112,7 +112,8 @@ struct fp_plan {
     double null_scale = 1.0;
     std::vector<PassT> passes;
     DevTables tab[3];
-    double* d_lam[3] = {nullptr, nullptr, nullptr};
+    double* d_lam[3] = {nullptr, nullptr, nullptr};       // per-axis eigenvalue tables
+    double* d_lam_pad[3] = {nullptr, nullptr, nullptr};   // the same, from the leading pad entry
     std::vector<void*> allocs;
     ~fp_plan() {
         int prev = 0;
@@ -241,13 +242,20 @@ fp_status validate(const fp_config* c) {
 
 // Which engine runs the transform along an axis, and its FFT length.
 // rfft: axis is the real-FFT periodic axis.  Returns M (0 = dense).
-int fft_length(int bc, int kind, long long n, bool rfft) {
+// complex FFT length of an axis on the FFT engine, 0 = dense engine
+int fft_length(int bc, int kind, long long n, bool rfft, bool regular_fft = true) {
     if (bc == FP_BC_PERIODIC) {
         const long long M = rfft ? ((n % 2 == 0) ? n / 2 : 0) : n;
         if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
         return 0;
     }
-    if (kind != FP_GRID_STAGGERED) return 0;  // DST-I / DCT-I: dense engine
+    if (kind != FP_GRID_STAGGERED) {
+        // DCT-I (n = M + 1) / DST-I (n = M - 1) as the real FFT of the 2M-point extension
+        if (!regular_fft) return 0;
+        const long long M = bc == FP_BC_NEUMANN ? n - 1 : n + 1;
+        if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+        return 0;
+    }
     if (n % 2) return 0;
     const long long M = n / 2;
     if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
@@ -322,7 +330,7 @@ static fp_status dist_layout(const fp_config* cfg, int nranks, DistLayout* L) {
     for (int a = 1; a < d; ++a) other_periodic |= cfg->bc[a] == FP_BC_PERIODIC;
     if (other_periodic && cfg->bc[0] != FP_BC_PERIODIC)
         return fail(FP_ERR_UNSUPPORTED, "distributed solve: with periodic axes other than 0, axis 0 must be periodic");
-    if (fft_length(cfg->bc[0], cfg->kind[0], cfg->n[0], cfg->bc[0] == FP_BC_PERIODIC && !other_periodic) == 0)
+    if (fft_length(cfg->bc[0], cfg->kind[0], cfg->n[0], cfg->bc[0] == FP_BC_PERIODIC && !other_periodic, false) == 0)
         return fail(FP_ERR_UNSUPPORTED, "distributed solve: axis 0 must be on the FFT engine (power-of-two length)");
     for (int a = 0; a < d; ++a)
         if (cfg->bc[a] == FP_BC_NEUMANN && cfg->kind[a] == FP_GRID_REGULAR)
@@ -428,24 +436,29 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         std::vector<double> lam;
         if (cfg->eig[a]) lam.assign(cfg->eig[a], cfg->eig[a] + cfg->n[a]);
         else lam = eigenvalue_table(AxisSpec{cfg->n[a], cfg->length[a], cfg->bc[a], cfg->kind[a]}, cfg->approx);
+        // one leading pad entry: a DST-I axis on the FFT engine reads its table from
+        // the pad (spectral index k = 1..M-1 <-> eigenvalue k - 1)
+        lam.insert(lam.begin(), 0.0);
         void* dl = nullptr;
         if (cudaMalloc(&dl, lam.size() * sizeof(double)) != cudaSuccess) { delete P; return fail(FP_ERR_ALLOC, "cudaMalloc eigenvalue table"); }
         P->allocs.push_back(dl);
         if (cudaMemcpy(dl, lam.data(), lam.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) { delete P; return fail(FP_ERR_CUDA, "upload eigenvalue table"); }
-        P->d_lam[a] = (double*)dl;
+        P->d_lam_pad[a] = (double*)dl;
+        P->d_lam[a] = (double*)dl + 1;
     }
 
     // per-axis engines + tables
     int Mx[3] = {0, 0, 0};
     for (int a = 0; a < d; ++a) {
         const bool rf = (a == P->r_axis);
-        Mx[a] = fft_length(cfg->bc[a], cfg->kind[a], cfg->n[a], rf);
+        Mx[a] = fft_length(cfg->bc[a], cfg->kind[a], cfg->n[a], rf, !dist);   // (slab phases: dense DCT-I/DST-I)
         DevTables& T = P->tab[a];
         if (Mx[a] > 0) {
             P->fft_mask |= 1 << a;
             std::vector<long double> wf, wt, ww;
             const bool real_kind = cfg->bc[a] != FP_BC_PERIODIC || rf;
-            fft_tables((int)cfg->n[a], Mx[a], real_kind, wf, wt, ww);
+            const bool regular = cfg->bc[a] != FP_BC_PERIODIC && cfg->kind[a] != FP_GRID_STAGGERED;
+            fft_tables(regular ? 2 * Mx[a] : (int)cfg->n[a], Mx[a], real_kind, wf, wt, ww);
             if ((st = upload(P->allocs, wf, P->f32, &T.wfft)) != FP_OK) { delete P; return st; }
             if ((st = upload(P->allocs, wt, P->f32, &T.wt)) != FP_OK) { delete P; return st; }
             if ((st = upload(P->allocs, ww, P->f32, &T.ww)) != FP_OK) { delete P; return st; }
@@ -498,8 +511,10 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         const bool periodic = cfg->bc[t] == FP_BC_PERIODIC;
         const bool rf = t == P->r_axis;
         p.op = op;
-        p.fkind = periodic ? (rf ? FK_RFFT : FK_CFFT) : (cfg->bc[t] == FP_BC_DIRICHLET ? FK_DST2 : FK_DCT2);
-        p.ikind = periodic ? (rf ? IK_IRFFT : IK_ICFFT) : (cfg->bc[t] == FP_BC_DIRICHLET ? IK_DST3 : IK_DCT3);
+        const bool regular = !periodic && cfg->kind[t] != FP_GRID_STAGGERED;
+        const bool dir = cfg->bc[t] == FP_BC_DIRICHLET;
+        p.fkind = periodic ? (rf ? FK_RFFT : FK_CFFT) : (regular ? (dir ? FK_DST1 : FK_DCT1) : (dir ? FK_DST2 : FK_DCT2));
+        p.ikind = periodic ? (rf ? IK_IRFFT : IK_ICFFT) : (regular ? (dir ? IK_DST1 : IK_DCT1) : (dir ? IK_DST3 : IK_DCT3));
         p.family = (t == d - 1) ? FAM_CONTIG : FAM_STRIDED;
         p.n = (int)cfg->n[t];
         p.M = Mx[t];
@@ -517,7 +532,8 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         p.ww = P->tab[t].ww;
         p.out_mult = 1.0;
         Scaling& s = p.s;
-        s.lam_t = P->d_lam[t];
+        // DST-I spectra sit at k = 1..M-1 of the extended line: eigenvalue k - 1
+        s.lam_t = (regular && dir) ? P->d_lam_pad[t] : P->d_lam[t];
         s.lam_a = ps.a >= 0 ? P->d_lam[ps.a] : nullptr;
         s.lam_b = ps.b >= 0 ? P->d_lam[ps.b] : nullptr;
         s.pos_t = t; s.pos_a = ps.a; s.pos_b = ps.b;
@@ -1045,12 +1061,15 @@ FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int dev
     long long M = 0;
     if (kind == FP_DFT || kind == FP_IDFT) M = n;
     else if (kind == FP_DST2 || kind == FP_DST3 || kind == FP_DCT2 || kind == FP_DCT3) M = (n % 2 == 0) ? n / 2 : 0;
+    else if (kind == FP_DCT1) M = n - 1;   // real FFT of the 2M-point even extension
+    else if (kind == FP_DST1) M = n + 1;   // ... of the odd extension
     T->fft = M >= 16 && M <= 4096 && is_pow2(M);
     fp_status st;
     if (T->fft) {
         T->M = (int)M;
         std::vector<long double> wf, wt, ww;
-        fft_tables((int)n, (int)M, !(kind == FP_DFT || kind == FP_IDFT), wf, wt, ww);
+        fft_tables((kind == FP_DCT1 || kind == FP_DST1) ? 2 * (int)M : (int)n, (int)M, !(kind == FP_DFT || kind == FP_IDFT),
+                   wf, wt, ww);
         if ((st = upload(T->allocs, wf, T->f32, &T->tab.wfft)) != FP_OK) { delete T; return st; }
         if ((st = upload(T->allocs, wt, T->f32, &T->tab.wt)) != FP_OK) { delete T; return st; }
         if ((st = upload(T->allocs, ww, T->f32, &T->tab.ww)) != FP_OK) { delete T; return st; }
@@ -1108,7 +1127,8 @@ FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int
         FftPass p{};
         const bool inv = T->kind == FP_IDFT || T->kind == FP_DST3 || T->kind == FP_DCT3;
         p.op = inv ? OP_INV : OP_FWD;
-        p.fkind = T->kind == FP_DFT ? FK_CFFT : (T->kind == FP_DST2 ? FK_DST2 : FK_DCT2);
+        p.fkind = T->kind == FP_DFT ? FK_CFFT
+                : T->kind == FP_DST2 ? FK_DST2 : T->kind == FP_DCT1 ? FK_DCT1 : T->kind == FP_DST1 ? FK_DST1 : FK_DCT2;
         p.ikind = T->kind == FP_IDFT ? IK_ICFFT : (T->kind == FP_DST3 ? IK_DST3 : IK_DCT3);
         p.family = (axis == ndim - 1) ? FAM_CONTIG : FAM_STRIDED;
         p.n = (int)T->n;

@@ -18,8 +18,10 @@ enum PassOp { OP_FWD = 0, OP_INV = 1, OP_MID = 2 };
 // Forward / inverse line kinds of the FFT engine (power-of-two lengths).
 // DCT2/DST2/RFFT are real-to-real/-complex transforms built around a
 // half-length complex FFT (Makhoul reordering + real-FFT untangling).
-enum FwdKind { FK_DCT2 = 0, FK_DST2 = 1, FK_RFFT = 2, FK_CFFT = 3 };
-enum InvKind { IK_DCT3 = 0, IK_DST3 = 1, IK_IRFFT = 2, IK_ICFFT = 3 };
+// DCT-I / DST-I (regular grids, n = 2^k +- 1) run as the half-length real FFT of the
+// even / odd extension (2M reals, M = n - 1 or n + 1); a pair's two kinds share a value
+enum FwdKind { FK_DCT2 = 0, FK_DST2 = 1, FK_RFFT = 2, FK_CFFT = 3, FK_DCT1 = 4, FK_DST1 = 5 };
+enum InvKind { IK_DCT3 = 0, IK_DST3 = 1, IK_IRFFT = 2, IK_ICFFT = 3, IK_DCT1 = 4, IK_DST1 = 5 };
 
 // Dense (direct-summation) engine classes, any length, any kind.
 enum DenseClass { DC_R2R = 0, DC_R2C = 1, DC_C2C = 2, DC_C2R = 3 };
