@@ -36,7 +36,7 @@ __all__ = [
     "PERIODIC", "DIRICHLET", "NEUMANN", "REGULAR", "STAGGERED", "SPECTRAL", "FD2",
     "Axis", "Case", "axis_dx", "axis_points", "eigenvalues", "pair", "backward_scale",
     "null_coeff", "forward_1d", "backward_1d", "naive_transform", "makhoul_dct2",
-    "makhoul_dct3", "solve", "laplacian", "dense_matrix", "dense_solve", "CONFIGS",
+    "makhoul_dct3", "r1_via_rfft", "r1_inverse_via_irfft", "solve", "laplacian", "dense_matrix", "dense_solve", "CONFIGS",
     "config_case", "config_rhs", "relative_l2",
 ]
 
@@ -227,6 +227,35 @@ def makhoul_dct3(X: np.ndarray) -> np.ndarray:
     x[..., 0::2] = v[..., :M]
     x[..., 1::2] = v[..., M:][..., ::-1]
     return x
+
+
+def r1_via_rfft(x: np.ndarray, kind: str) -> np.ndarray:
+    """DCT-I / DST-I as the real FFT of the even / odd 2M-point extension (the
+    recipe of the sm_100a kernels for regular grids; the reference computes them
+    with scipy.fft.dct/dst type 1, transforms.py:70-77).
+
+    DCT-I (n = M + 1): z = [x_0..x_M, x_{M-1}..x_1], X_k = Re rfft(z)_k.
+    DST-I (n = M - 1): z = [0, x, 0, -reverse(x)],   X_{k-1} = -Im rfft(z)_k.
+    """
+    if kind == "dct1":
+        z = np.concatenate([x, x[..., -2:0:-1]], axis=-1)
+        return np.fft.rfft(z, axis=-1).real
+    zero = np.zeros(x.shape[:-1] + (1,))
+    z = np.concatenate([zero, x, zero, -x[..., ::-1]], axis=-1)
+    return -np.fft.rfft(z, axis=-1).imag[..., 1:-1]
+
+
+def r1_inverse_via_irfft(X: np.ndarray, kind: str) -> np.ndarray:
+    """The unnormalised DCT-I / DST-I of X computed as the inverse real FFT of the
+    half spectrum (X_k, 0) resp. (0, -X_{k-1}), truncated to n outputs (the
+    kernels' inverse / second leg of the fused middle pass)."""
+    if kind == "dct1":
+        M = X.shape[-1] - 1
+        return (np.fft.irfft(X.astype(complex), n=2 * M, axis=-1) * (2 * M))[..., : M + 1]
+    M = X.shape[-1] + 1
+    S = np.zeros(X.shape[:-1] + (M + 1,), dtype=complex)
+    S[..., 1:M] = -1j * X
+    return (np.fft.irfft(S, n=2 * M, axis=-1) * (2 * M))[..., 1:M]
 
 
 # -- solver.py:136-249 -----------------------------------------------------------

@@ -77,6 +77,17 @@ def test_makhoul_recipes_match_scipy(n, rng):
     np.testing.assert_allclose(s * orc.makhoul_dct3(x[..., ::-1]), orc.forward_1d("dst3", x), atol=1e-12 * n)
 
 
+@pytest.mark.parametrize("M", [16, 32, 256])
+def test_regular_grid_recipes_match_scipy(M, rng):
+    # DCT-I / DST-I via the real FFT of the extension (the FFT-engine recipe for
+    # regular grids) against scipy's type-1 transforms, forward and inverse legs
+    for kind, n in (("dct1", M + 1), ("dst1", M - 1)):
+        x = rng.standard_normal((3, n))
+        want = orc.forward_1d(kind, x)
+        np.testing.assert_allclose(orc.r1_via_rfft(x, kind), want, atol=1e-12 * n)
+        np.testing.assert_allclose(orc.r1_inverse_via_irfft(x, kind), want, atol=1e-12 * n)
+
+
 def test_known_answers_transforms():
     # reference tests/test_transforms.py:55-94
     np.testing.assert_allclose(orc.forward_1d("dst1", np.array([1.0, 0.0])), [math.sqrt(3), math.sqrt(3)], atol=1e-14)
