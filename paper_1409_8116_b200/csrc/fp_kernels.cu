@@ -25,9 +25,11 @@
 //   N-element array (solver.py:149-159), which would cost N*8 extra bytes.
 //
 // Dense engine: direct summation with a host-built, correctly rounded matrix
-//   for every other (kind, n) the reference supports (DST-I, DCT-I, odd n,
-//   tiny n).  Tile-exclusive, so in-place safe.
+//   for every other (kind, n) the reference supports (odd n, tiny n, ...):
+//   a register-tiled product for lines of 64+ points, a simple one for short
+//   lines.  Both tile-exclusive (a CTA owns complete lines), so in-place safe.
 #include <cstdlib>
+#include <type_traits>
 
 #include "fp_common.cuh"
 
@@ -38,6 +40,109 @@ FftKernelFn pick_fft_d_lo(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_d_hi(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_f_lo(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_f_hi(int logM, bool strided, int op, bool pipe, int kind);
+
+// ----------------------------------------------------------------------------
+// dense engine, long lines: the same product as a register-tiled GEMM.  The CTA
+// still owns LT complete lines (staged in shared memory first, so in-place
+// passes stay safe); the matrix streams through a padded [JT][KT] shared tile,
+// and every thread accumulates KB outputs for all LT lines (the line values are
+// warp-wide broadcast reads).  The matrix is read once per LT lines instead of
+// once per line.
+template <typename T, int CLS, int LT>
+__global__ void __launch_bounds__(256) dense_tile_kernel(const DensePass p) {
+    constexpr bool CIN = CLS == DC_C2C || CLS == DC_C2R;
+    constexpr bool CMAT = CLS != DC_R2R;
+    constexpr bool COUT = CLS == DC_C2C || CLS == DC_R2C;
+    constexpr int KB = 2, JT = 8, KT = 256 * KB, AS = KT + 1;   // odd row stride: conflict-free staging
+    using XE = typename std::conditional<CIN, cx<T>, T>::type;
+    using ME = typename std::conditional<CMAT, cx<T>, T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nin = p.n_in, nout = p.n_out;
+    XE* xs = reinterpret_cast<XE*>(smem_raw);
+    ME* as = reinterpret_cast<ME*>(smem_raw + (((size_t)LT * nin * sizeof(XE) + 15) & ~(size_t)15));
+    const Geometry& g = p.g;
+    const int tid = threadIdx.x;
+    const long long nlines = (long long)g.na * g.nb;
+    const long long l0 = (long long)blockIdx.x * LT;
+    int nonfinite = 0;
+    for (int idx = tid; idx < LT * nin; idx += 256) {
+        const int li = idx / nin, j = idx - li * nin;
+        const long long l = l0 + li;
+        XE v;
+        if constexpr (CIN) v = mkc<T>(0, 0); else v = (T)0;
+        if (l < nlines) {
+            const long long off = (l / g.nb) * g.in_sa + (l % g.nb) * g.in_sb + (long long)j * g.in_st;
+            if constexpr (CIN) {
+                v = ld_cx<T>(g.in, g.in_type, off);
+                if (p.nonfinite && !(finite_t(v.x) && finite_t(v.y))) nonfinite = 1;
+            } else {
+                v = ld_real<T>(g.in, g.in_type, off);
+                if (p.nonfinite && !finite_t(v)) nonfinite = 1;
+            }
+        }
+        xs[idx] = v;
+    }
+    if (nonfinite) *p.nonfinite = 1;
+    const ME* mat = reinterpret_cast<const ME*>(p.mat);
+    const T om = (T)p.out_mult;
+    for (int k0 = 0; k0 < nout; k0 += KT) {
+        T ar[LT][KB], ai[LT][KB];
+#pragma unroll
+        for (int l = 0; l < LT; ++l)
+#pragma unroll
+            for (int b = 0; b < KB; ++b) ar[l][b] = ai[l][b] = (T)0;
+        for (int j0 = 0; j0 < nin; j0 += JT) {
+            __syncthreads();   // (first round: the staged lines; later: the previous matrix tile is consumed)
+            for (int idx = tid; idx < KT * JT; idx += 256) {
+                const int kk = idx / JT, jj = idx - kk * JT;
+                const int k = k0 + kk, j = j0 + jj;
+                ME m;
+                if constexpr (CMAT) m = mkc<T>(0, 0); else m = (T)0;
+                if (k < nout && j < nin) m = __ldg(&mat[(long long)k * nin + j]);
+                as[jj * AS + kk] = m;
+            }
+            __syncthreads();
+            const int jn = min(JT, nin - j0);
+            for (int jj = 0; jj < jn; ++jj) {
+                ME a[KB];
+#pragma unroll
+                for (int b = 0; b < KB; ++b) a[b] = as[jj * AS + tid + 256 * b];
+#pragma unroll
+                for (int l = 0; l < LT; ++l) {
+                    const XE x = xs[l * nin + j0 + jj];
+#pragma unroll
+                    for (int b = 0; b < KB; ++b) {
+                        if constexpr (CLS == DC_R2R) {
+                            ar[l][b] = fma(a[b], x, ar[l][b]);
+                        } else if constexpr (CLS == DC_R2C) {
+                            ar[l][b] = fma(a[b].x, x, ar[l][b]);
+                            ai[l][b] = fma(a[b].y, x, ai[l][b]);
+                        } else if constexpr (CLS == DC_C2C) {
+                            ar[l][b] = fma(a[b].x, x.x, fma(-a[b].y, x.y, ar[l][b]));
+                            ai[l][b] = fma(a[b].x, x.y, fma(a[b].y, x.x, ai[l][b]));
+                        } else {   // C2R: Re(sum m_j X_j)
+                            ar[l][b] = fma(a[b].x, x.x, fma(-a[b].y, x.y, ar[l][b]));
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < LT; ++l) {
+            const long long ll = l0 + l;
+            if (ll >= nlines) break;
+            const long long ob = (ll / g.nb) * g.out_sa + (ll % g.nb) * g.out_sb;
+#pragma unroll
+            for (int b = 0; b < KB; ++b) {
+                const int k = k0 + tid + 256 * b;
+                if (k >= nout) continue;
+                const long long off = ob + (long long)k * g.out_st;
+                if constexpr (COUT) st_cx<T>(g.out, g.out_type, off, mkc<T>(ar[l][b] * om, ai[l][b] * om));
+                else st_real<T>(g.out, g.out_type, off, ar[l][b] * om);
+            }
+        }
+    }
+}
 
 // ----------------------------------------------------------------------------
 // dense engine: out_k = sum_j mat[k][j] * in_j, one tile of lines per CTA
@@ -341,9 +446,54 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+template <typename T, int CLS, int LT>
+static cudaError_t launch_dense_tile_lt(const DensePass& p, size_t smem, long long tiles, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(dense_tile_kernel<T, CLS, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    dense_tile_kernel<T, CLS, LT><<<(unsigned)tiles, 256, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename T, int CLS>
+static cudaError_t launch_dense_tile(const DensePass& p, cudaStream_t st) {
+    const bool cin = CLS == DC_C2C || CLS == DC_C2R;
+    const size_t xe = (cin ? 2 : 1) * sizeof(T), me = (CLS != DC_R2R ? 2 : 1) * sizeof(T);
+    const size_t as_bytes = (size_t)8 * (512 + 1) * me;
+    const long long nlines = (long long)p.g.na * p.g.nb;
+    int lt = 8;   // lines per CTA: as many as fit next to the matrix tile
+    while (lt > 1 && (((size_t)lt * p.n_in * xe + 15) & ~(size_t)15) + as_bytes > 200 * 1024) lt >>= 1;
+    while (lt > 1 && lt / 2 >= nlines) lt >>= 1;
+    const size_t smem = (((size_t)lt * p.n_in * xe + 15) & ~(size_t)15) + as_bytes;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const long long tiles = (nlines + lt - 1) / lt;
+    switch (lt) {
+        case 8: return launch_dense_tile_lt<T, CLS, 8>(p, smem, tiles, st);
+        case 4: return launch_dense_tile_lt<T, CLS, 4>(p, smem, tiles, st);
+        case 2: return launch_dense_tile_lt<T, CLS, 2>(p, smem, tiles, st);
+        default: return launch_dense_tile_lt<T, CLS, 1>(p, smem, tiles, st);
+    }
+}
+
+template <typename T>
+static cudaError_t launch_dense_tile_cls(const DensePass& p, cudaStream_t st) {
+    switch (p.cls) {
+        case DC_R2R: return launch_dense_tile<T, DC_R2R>(p, st);
+        case DC_R2C: return launch_dense_tile<T, DC_R2C>(p, st);
+        case DC_C2C: return launch_dense_tile<T, DC_C2C>(p, st);
+        default: return launch_dense_tile<T, DC_C2R>(p, st);
+    }
+}
+
 cudaError_t launch_dense_pass(const DensePass& p, bool f32, cudaStream_t st) {
     cudaError_t e = set_smem_attr();
     if (e != cudaSuccess) return e;
+    static const int tile_min = [] { const char* v = getenv("FP_DENSE_TILE_MIN"); return (v && *v) ? atoi(v) : 64; }();
+    if (p.n_in >= tile_min) return f32 ? launch_dense_tile_cls<float>(p, st) : launch_dense_tile_cls<double>(p, st);
     const size_t smem = (size_t)p.lines * p.in_ls * (f32 ? 4 : 8);
     if (f32) dense_pass_kernel<float><<<p.tiles, 256, smem, st>>>(p);
     else dense_pass_kernel<double><<<p.tiles, 256, smem, st>>>(p);

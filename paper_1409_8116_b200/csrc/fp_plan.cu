@@ -162,6 +162,26 @@ int ilog2(long long x) { int l = 0; while ((1LL << l) < x) ++l; return l; }
 
 // upload a long double table rounded to the plan precision (complex pairs or reals)
 template <typename AllocT>
+fp_status upload(AllocT& allocs, const std::vector<double>& v, bool f32, void** out) {
+    *out = nullptr;
+    if (v.empty()) return FP_OK;
+    const size_t cnt = v.size();
+    void* d = nullptr;
+    if (f32) {
+        std::vector<float> h(cnt);
+        for (size_t i = 0; i < cnt; ++i) h[i] = (float)v[i];
+        CUDA_TRY(cudaMalloc(&d, cnt * sizeof(float)));
+        allocs.push_back(d);
+        CUDA_TRY(cudaMemcpy(d, h.data(), cnt * sizeof(float), cudaMemcpyHostToDevice));
+    } else {
+        CUDA_TRY(cudaMalloc(&d, cnt * sizeof(double)));
+        allocs.push_back(d);
+        CUDA_TRY(cudaMemcpy(d, v.data(), cnt * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    *out = d;
+    return FP_OK;
+}
+template <typename AllocT>
 fp_status upload(AllocT& allocs, const std::vector<long double>& v, bool f32, void** out) {
     *out = nullptr;
     if (v.empty()) return FP_OK;
@@ -262,7 +282,9 @@ int fft_length(int bc, int kind, long long n, bool rfft, bool regular_fft = true
     return 0;
 }
 
-const long long kDenseMax = 4096;
+// longest dense-engine line: the register-tiled kernel stages one line next to
+// its matrix tile (complex fp64 fits up to 8695 points); the matrix is n^2 entries
+const long long kDenseMax = 8192;
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -466,9 +488,9 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             if (cfg->n[a] > kDenseMax) {
                 delete P;
                 return fail(FP_ERR_UNSUPPORTED, "axis length " + std::to_string(cfg->n[a]) +
-                                                    " needs the dense engine, limited to n <= 4096 in this build");
+                                                    " needs the dense engine, limited to n <= 8192 in this build");
             }
-            std::vector<long double> m;
+            std::vector<double> m;
             int no, ni;
             bool cpx;
             const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
@@ -1074,8 +1096,8 @@ FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int dev
         if ((st = upload(T->allocs, wt, T->f32, &T->tab.wt)) != FP_OK) { delete T; return st; }
         if ((st = upload(T->allocs, ww, T->f32, &T->tab.ww)) != FP_OK) { delete T; return st; }
     } else {
-        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length needs the dense engine (n <= 4096)"); }
-        std::vector<long double> m;
+        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length needs the dense engine (n <= 8192)"); }
+        std::vector<double> m;
         int no, ni;
         bool cpx;
         dense_matrix(kind, (int)n, m, &no, &ni, &cpx);

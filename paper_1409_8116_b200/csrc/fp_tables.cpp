@@ -132,64 +132,94 @@ std::vector<double> eigenvalue_table(const AxisSpec& a, int approx) {
 
 // Dense matrices, row-major [n_out][n_in]; complex ones interleaved (re, im).
 // kind uses the public FP_* transform ids.
-bool dense_matrix(int kind, int n, std::vector<long double>& m, int* n_out, int* n_in, bool* cpx) {
+// every entry of a dense matrix is cis(2 pi num / den) for one den per kind: the
+// den roots are computed once (correctly rounded via exact_cis) and looked up,
+// so building an n x n matrix costs O(den) trig calls instead of O(n^2)
+namespace {
+struct Roots {
+    long long den;
+    std::vector<long double> c, s;
+    explicit Roots(long long d) : den(d), c((size_t)d), s((size_t)d) {
+        for (long long q = 0; q < d; ++q) exact_cis(q, d, &c[(size_t)q], &s[(size_t)q]);
+    }
+    void get(long long num, long double* cc, long double* ss) const {
+        num %= den;
+        if (num < 0) num += den;
+        *cc = c[(size_t)num];
+        *ss = s[(size_t)num];
+    }
+};
+}  // namespace
+
+bool dense_matrix(int kind, int n, std::vector<double>& m, int* n_out, int* n_in, bool* cpx) {
     m.clear();
     long double c, s;
     if (kind == 0 || kind == 1) {  // DFT / IDFT (unnormalized here)
         *n_out = n; *n_in = n; *cpx = true;
-        m.assign(2 * (size_t)n * n, 0.0L);
+        m.assign(2 * (size_t)n * n, 0.0);
+        const Roots r(n);
         for (int k = 0; k < n; ++k)
             for (int j = 0; j < n; ++j) {
-                exact_cis((long long)k * j, n, &c, &s);
-                m[2 * ((size_t)k * n + j)] = c;
-                m[2 * ((size_t)k * n + j) + 1] = kind == 0 ? -s : s;
+                r.get((long long)k * j, &c, &s);
+                m[2 * ((size_t)k * n + j)] = (double)c;
+                m[2 * ((size_t)k * n + j) + 1] = (double)(kind == 0 ? -s : s);
             }
         return true;
     }
     if (kind == 100) {  // real-input DFT, outputs k = 0..n/2
         const int h = n / 2 + 1;
         *n_out = h; *n_in = n; *cpx = true;
-        m.assign(2 * (size_t)h * n, 0.0L);
+        m.assign(2 * (size_t)h * n, 0.0);
+        const Roots r(n);
         for (int k = 0; k < h; ++k)
             for (int j = 0; j < n; ++j) {
-                exact_cis((long long)k * j, n, &c, &s);
-                m[2 * ((size_t)k * n + j)] = c;
-                m[2 * ((size_t)k * n + j) + 1] = -s;
+                r.get((long long)k * j, &c, &s);
+                m[2 * ((size_t)k * n + j)] = (double)c;
+                m[2 * ((size_t)k * n + j) + 1] = (double)-s;
             }
         return true;
     }
     if (kind == 101) {  // Hermitian half-spectrum -> real, unnormalized inverse
         const int h = n / 2 + 1;
         *n_out = n; *n_in = h; *cpx = true;
-        m.assign(2 * (size_t)n * h, 0.0L);
+        m.assign(2 * (size_t)n * h, 0.0);
+        const Roots r(n);
         for (int j = 0; j < n; ++j)
             for (int k = 0; k < h; ++k) {
                 long double w = 2.0L;
                 if (k == 0 || (n % 2 == 0 && k == n / 2)) w = 1.0L;
-                exact_cis((long long)j * k, n, &c, &s);
-                m[2 * ((size_t)j * h + k)] = w * c;
-                m[2 * ((size_t)j * h + k) + 1] = w * s;
+                r.get((long long)j * k, &c, &s);
+                m[2 * ((size_t)j * h + k)] = (double)(w * c);
+                m[2 * ((size_t)j * h + k) + 1] = (double)(w * s);
             }
         return true;
     }
     *n_out = n; *n_in = n; *cpx = false;
-    m.assign((size_t)n * n, 0.0L);
+    long long den;
+    switch (kind) {
+        case 2: den = 2LL * (n + 1); break;          // DST1
+        case 3: case 4: case 6: case 7: den = 4LL * n; break;
+        case 5: den = 2LL * (n > 1 ? n - 1 : 1); break;   // DCT1
+        default: return false;
+    }
+    const Roots r(den);
+    m.assign((size_t)n * n, 0.0);
     for (int k = 0; k < n; ++k) {
         for (int j = 0; j < n; ++j) {
             long double val = 0.0L;
             switch (kind) {
                 case 2:  // DST1: 2 sin(pi (j+1)(k+1)/(n+1))
-                    exact_cis((long long)(j + 1) * (k + 1), 2LL * (n + 1), &c, &s);
+                    r.get((long long)(j + 1) * (k + 1), &c, &s);
                     val = 2.0L * s;
                     break;
                 case 3:  // DST2: 2 sin(pi (j+1/2)(k+1)/n)
-                    exact_cis((long long)(2 * j + 1) * (k + 1), 4LL * n, &c, &s);
+                    r.get((long long)(2 * j + 1) * (k + 1), &c, &s);
                     val = 2.0L * s;
                     break;
                 case 4:  // DST3: 2 sin(pi (j+1)(k+1/2)/n); column n-1: (-1)^k
                     if (j == n - 1) val = (k % 2 == 0) ? 1.0L : -1.0L;
                     else {
-                        exact_cis((long long)(j + 1) * (2 * k + 1), 4LL * n, &c, &s);
+                        r.get((long long)(j + 1) * (2 * k + 1), &c, &s);
                         val = 2.0L * s;
                     }
                     break;
@@ -197,25 +227,23 @@ bool dense_matrix(int kind, int n, std::vector<long double>& m, int* n_out, int*
                     if (j == 0) val = 1.0L;
                     else if (j == n - 1) val = (k % 2 == 0) ? 1.0L : -1.0L;
                     else {
-                        exact_cis((long long)j * k, 2LL * (n - 1), &c, &s);
+                        r.get((long long)j * k, &c, &s);
                         val = 2.0L * c;
                     }
                     break;
                 case 6:  // DCT2: 2 cos(pi (j+1/2) k/n)
-                    exact_cis((long long)(2 * j + 1) * k, 4LL * n, &c, &s);
+                    r.get((long long)(2 * j + 1) * k, &c, &s);
                     val = 2.0L * c;
                     break;
-                case 7:  // DCT3: 2 cos(pi j (k+1/2)/n); column 0: 1
+                default:  // 7, DCT3: 2 cos(pi j (k+1/2)/n); column 0: 1
                     if (j == 0) val = 1.0L;
                     else {
-                        exact_cis((long long)j * (2 * k + 1), 4LL * n, &c, &s);
+                        r.get((long long)j * (2 * k + 1), &c, &s);
                         val = 2.0L * c;
                     }
                     break;
-                default:
-                    return false;
             }
-            m[(size_t)k * n + j] = val;
+            m[(size_t)k * n + j] = (double)val;
         }
     }
     return true;

@@ -17,6 +17,6 @@ void fft_tables(int n_real, int M, bool real_kind, std::vector<long double>& wff
 double axis_dx(const AxisSpec& a);
 std::vector<double> eigenvalue_table(const AxisSpec& a, int approx);
 // kind: FP_DFT..FP_DCT3, or 100 (real-input DFT half spectrum), 101 (half spectrum -> real)
-bool dense_matrix(int kind, int n, std::vector<long double>& m, int* n_out, int* n_in, bool* cpx);
+bool dense_matrix(int kind, int n, std::vector<double>& m, int* n_out, int* n_in, bool* cpx);
 
 }  // namespace fpb
