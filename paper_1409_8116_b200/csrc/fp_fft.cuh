@@ -12,6 +12,7 @@
 //     line), STRIDED = column-major (lanes walk across the W adjacent lines so
 //     each row segment of W elements is one coalesced access).
 #pragma once
+#include <cstdlib>
 #include <type_traits>
 
 #include "fp_common.cuh"
@@ -1276,6 +1277,19 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     fft_pass_tile<T, LOGM, STRIDED, OP>(p);
 }
 
+// Long fp32 strided forward / inverse lines: at <= 64 registers two 512-thread
+// CTAs fit per SM (70 would allow one).
+#ifndef FP_WIDE_F32_REGS
+#define FP_WIDE_F32_REGS 64
+#endif
+#ifndef FP_WIDE_F32_MID
+#define FP_WIDE_F32_MID 0   // the MID too (variant builds; it spills at 64)
+#endif
+template <typename T, int LOGM, int OP>
+__global__ void __maxnreg__(FP_WIDE_F32_REGS) fft_pass_wide_f32(const FftPass p) {
+    fft_pass_tile<T, LOGM, true, OP>(p);
+}
+
 // Contiguous tiles trade registers for residency: capped at 72 (fp32) / 96 (fp64)
 // they run 5-7 CTAs/SM instead of 4 (c5 line passes 16.5 -> 14.4 ms; c3 -2 %).
 #ifndef FP_CONTIG_REGS_F32
@@ -1389,6 +1403,17 @@ __global__ void __launch_bounds__(512) fft_pass_spipe(const FftPass p) {
     }
 }
 
+inline bool wide_f32_enabled() {
+    static const bool on = [] { const char* v = std::getenv("FP_WIDE_F32"); return !(v && *v == '0'); }();
+    return on;
+}
+// strided entry point of (T, L, OPV): the 64-register one for long fp32 lines
+template <typename T, int L, int OPV>
+inline FftKernelFn strided_fn() {
+    if constexpr (sizeof(T) == 4 && L >= 9 && (opb(OPV) != OP_MID || FP_WIDE_F32_MID))
+        if (wide_f32_enabled()) return fft_pass_wide_f32<T, L, OPV>;
+    return fft_pass_kernel<T, L, true, OPV>;
+}
 template <typename T, int L, int OPV>
 inline FftKernelFn spipe_fn(bool strided) {
     if constexpr (opb(OPV) == OP_MID) return nullptr;   // the MID step is not pipelined
@@ -1406,19 +1431,19 @@ inline FftKernelFn spipe_fn(bool strided) {
     namespace fpb {                                                                                   \
     template <int L, int OPV> static FftKernelFn NAME##_one(bool s, bool pipe) {                      \
         if (pipe) return FP_FFT_PIPE_FN(T, L, s, OPV);                                                \
-        return s ? fft_pass_kernel<T, L, true, OPV> : fft_pass_contig<T, L, OPV>;                     \
+        return s ? strided_fn<T, L, OPV>() : fft_pass_contig<T, L, OPV>;                              \
     }                                                                                                 \
     template <int L> static FftKernelFn NAME##_mid(bool s, bool pipe, int kind) {                     \
         if (pipe || !s || kind < 0) return NAME##_one<L, OP_MID>(s, pipe);                            \
         switch (kind) {                                                                               \
-            case FK_DCT2: return fft_pass_kernel<T, L, true, mid_op(FK_DCT2)>;                        \
-            case FK_DST2: return fft_pass_kernel<T, L, true, mid_op(FK_DST2)>;                        \
-            case FK_RFFT: return fft_pass_kernel<T, L, true, mid_op(FK_RFFT)>;                        \
-            case FK_DCT1: return fft_pass_kernel<T, L, true, mid_op(FK_DCT1)>;                        \
-            case FK_DST1: return fft_pass_kernel<T, L, true, mid_op(FK_DST1)>;                        \
+            case FK_DCT2: return strided_fn<T, L, mid_op(FK_DCT2)>();                        \
+            case FK_DST2: return strided_fn<T, L, mid_op(FK_DST2)>();                        \
+            case FK_RFFT: return strided_fn<T, L, mid_op(FK_RFFT)>();                        \
+            case FK_DCT1: return strided_fn<T, L, mid_op(FK_DCT1)>();                        \
+            case FK_DST1: return strided_fn<T, L, mid_op(FK_DST1)>();                        \
             default: /* fp64 complex: the specialised build spills (c4 MID +7 %) */                  \
                 if constexpr (sizeof(T) == 8) return NAME##_one<L, OP_MID>(s, pipe);                  \
-                else return fft_pass_kernel<T, L, true, mid_op(FK_CFFT)>;                             \
+                else return strided_fn<T, L, mid_op(FK_CFFT)>();                             \
         }                                                                                             \
     }                                                                                                 \
     template <int L> static FftKernelFn NAME##_rec(int logM, bool s, int op, bool pipe, int kind) {   \
