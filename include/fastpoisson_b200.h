@@ -22,6 +22,9 @@
  *   fp_transform_execute TransformPlan.execute_real/_complex transforms.py:157-172
  *   fp_last_error       exception message of the failing call
  *   fp_event_*          CUDA events behind SolveReport.timing (solver.py:215-228)
+ *   fp_solve_divergence ProjectionFlow stage: rhs = divergence(star)/(alpha dt),
+ *                       poisson.solve(rhs)              flow.py:114-122, 290-291
+ *   fp_project_correct  u, w -= alpha dt gradient(phi); p += phi   flow.py:125-139, 292-295
  *   fp_plan_create_dist / fp_solve_phase / fp_dist_layout
  *                       slab-decomposed solve over P ranks (the paper's MPI
  *                       global transposes; the reorder seam
@@ -173,6 +176,25 @@ FP_API fp_status fp_transform_execute(const fp_transform* t, int ndim, const int
                                       const void* in, int in_dtype, const int64_t* in_strides,
                                       void* out, int out_dtype, const int64_t* out_strides,
                                       void* stream);
+
+/* ---- projection step of the 2D staggered-grid flow (flow.py:284-295) ----------
+ * For the flow's plan (axis 0 = x periodic; axis 1 = z periodic or staggered
+ * Neumann walls), with cells (nx, nz), u on x-faces (nx, nz), w on z-faces (nx, nz)
+ * periodic / (nx, nz + 1) walls, all plan-typed device arrays:
+ *   fp_solve_divergence: phi = solve(div(u, w) / scale); the divergence is formed by
+ *     the first pass while it loads its lines (no rhs array), or by a stand-alone
+ *     kernel when the z axis is on the dense engine.  Same workspace / dev_info /
+ *     stream rules as fp_solve.  NULL strides = dense C order.
+ *   fp_project_correct: u_out = u_star - scale * d_x phi, w_out = w_star - scale * d_z phi
+ *     (wall faces keep w_star), p_inout += phi if non-NULL; dense arrays, in place allowed. */
+FP_API fp_status fp_solve_divergence(const fp_plan* plan, const void* u, const int64_t* u_strides,
+                                     const void* w, const int64_t* w_strides, double scale,
+                                     void* phi, const int64_t* phi_strides,
+                                     void* workspace, size_t workspace_bytes, void* stream,
+                                     fp_solve_info* dev_info);
+FP_API fp_status fp_project_correct(const fp_plan* plan, const void* phi, const void* u_star,
+                                    const void* w_star, void* u_out, void* w_out, void* p_inout,
+                                    double scale, void* stream);
 
 /* ---- slab decomposition over P ranks (axis 0 split; one all-to-all each way) ----
  * Rank r owns planes [r*local_n0, (r+1)*local_n0) of axis 0 (local arrays are

@@ -36,7 +36,8 @@ __all__ = [
     "PERIODIC", "DIRICHLET", "NEUMANN", "REGULAR", "STAGGERED", "SPECTRAL", "FD2",
     "Axis", "Case", "axis_dx", "axis_points", "eigenvalues", "pair", "backward_scale",
     "null_coeff", "forward_1d", "backward_1d", "naive_transform", "makhoul_dct2",
-    "makhoul_dct3", "r1_via_rfft", "r1_inverse_via_irfft", "solve", "laplacian", "dense_matrix", "dense_solve", "CONFIGS",
+    "makhoul_dct3", "r1_via_rfft", "r1_inverse_via_irfft", "staggered_divergence", "staggered_gradient",
+    "projection_case", "project_step", "solve", "laplacian", "dense_matrix", "dense_solve", "CONFIGS",
     "config_case", "config_rhs", "relative_l2",
 ]
 
@@ -256,6 +257,48 @@ def r1_inverse_via_irfft(X: np.ndarray, kind: str) -> np.ndarray:
     S = np.zeros(X.shape[:-1] + (M + 1,), dtype=complex)
     S[..., 1:M] = -1j * X
     return (np.fft.irfft(S, n=2 * M, axis=-1) * (2 * M))[..., 1:M]
+
+
+# -- flow.py: the projection step around the solve ---------------
+def staggered_divergence(u: np.ndarray, w: np.ndarray, lengths, z_walls: bool) -> np.ndarray:
+    """Cell-centred divergence of face velocities (flow.py:114-122)."""
+    nx, nz = u.shape
+    dx, dz = lengths[0] / nx, lengths[1] / nz
+    div = (np.roll(u, -1, axis=0) - u) / dx
+    if z_walls:
+        div += (w[:, 1:] - w[:, :-1]) / dz
+    else:
+        div += (np.roll(w, -1, axis=1) - w) / dz
+    return div
+
+
+def staggered_gradient(phi: np.ndarray, lengths, z_walls: bool):
+    """Face gradient of a cell-centred scalar; wall faces get 0 (flow.py:125-139)."""
+    nx, nz = phi.shape
+    dx, dz = lengths[0] / nx, lengths[1] / nz
+    gx = (phi - np.roll(phi, 1, axis=0)) / dx
+    if z_walls:
+        gz = np.zeros((nx, nz + 1))
+        gz[:, 1:-1] = (phi[:, 1:] - phi[:, :-1]) / dz
+    else:
+        gz = (phi - np.roll(phi, 1, axis=1)) / dz
+    return gx, gz
+
+
+def projection_case(cells, lengths, z_walls: bool) -> "Case":
+    """The flow's pressure plan (flow.py:241-250)."""
+    nx, nz = cells
+    zax = (nz, lengths[1], NEUMANN, STAGGERED) if z_walls else (nz, lengths[1], PERIODIC)
+    return Case([(nx, lengths[0], PERIODIC), zax], FD2)
+
+
+def project_step(ustar, wstar, scale, lengths, z_walls: bool):
+    """One projection of a ProjectionFlow stage (flow.py:290-295) -> (u, w, phi)."""
+    case = projection_case(ustar.shape, lengths, z_walls)
+    rhs = staggered_divergence(ustar, wstar, lengths, z_walls) / scale
+    phi, _ = solve(case, rhs)
+    gx, gz = staggered_gradient(phi, lengths, z_walls)
+    return ustar - scale * gx, wstar - scale * gz, phi
 
 
 # -- solver.py:136-249 -----------------------------------------------------------

@@ -18,8 +18,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB_PATH = LIB_DIR / "libfastpoisson_b200.so"
 
-SOURCES = ["fp_fft_d_hi.cu", "fp_fft_d_lo.cu", "fp_fft_f_hi.cu", "fp_fft_f_lo.cu",
-           "fp_kernels.cu", "fp_plan.cu", "fp_tables.cpp"]
+SOURCES = [f"fp_fft_{t}_l{g}.cu" for t in ("d", "f") for g in (4, 6, 8, 9, 11, 12)] + [
+    "fp_kernels.cu", "fp_plan.cu", "fp_tables.cpp"]
 HEADERS = ["fp_types.h", "fp_tables.h", "fp_common.cuh", "fp_fft.cuh"]
 OBJ_DIR = PKG / "build"
 

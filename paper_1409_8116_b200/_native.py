@@ -103,6 +103,15 @@ SIGNATURES = {
         [c_void_p, c_int, POINTER(c_int64), c_int, c_void_p, c_int, POINTER(c_int64), c_void_p, c_int,
          POINTER(c_int64), c_void_p],
     ),
+    "fp_solve_divergence": (
+        c_int,
+        [c_void_p, c_void_p, POINTER(c_int64), c_void_p, POINTER(c_int64), c_double, c_void_p, POINTER(c_int64),
+         c_void_p, c_size_t, c_void_p, c_void_p],
+    ),
+    "fp_project_correct": (
+        c_int,
+        [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_void_p],
+    ),
     "fp_dist_layout": (c_int, [POINTER(FpConfig), c_int, c_int, POINTER(FpDistInfo)]),
     "fp_plan_create_dist": (c_int, [POINTER(FpConfig), c_int, c_int, c_int, POINTER(c_void_p)]),
     "fp_solve_phase": (

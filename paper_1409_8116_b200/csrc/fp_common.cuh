@@ -298,7 +298,7 @@ template <typename T> __device__ __forceinline__ bool finite_t(T x) { return isf
 struct LineInfo {
     long long in_off, out_off;
     double before, after1, after2;  // eigenvalue partial sums (axis order)
-    int nafter, valid, null_line, pad;
+    int nafter, valid, null_line, lb;   // lb: global line index along b (rhs producers)
 };
 // the line table is padded so the complex tile behind it is 16-byte aligned
 __host__ __device__ __forceinline__ size_t linfo_bytes(int lines) {

@@ -102,7 +102,7 @@ __device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo
         if (ha && p.s.pos_a > p.s.pos_t) { a1 = la; nafter = 1; }
         if (hb && p.s.pos_b > p.s.pos_t) { if (nafter == 0) a1 = lb; else a2 = lb; ++nafter; }
     }
-    L.before = before; L.after1 = a1; L.after2 = a2; L.nafter = nafter; L.pad = 0;
+    L.before = before; L.after1 = a1; L.after2 = a2; L.nafter = nafter; L.lb = ibg;
     linfo[tid] = L;
 }
 
@@ -172,6 +172,33 @@ __device__ __forceinline__ void load_pairs(cx<T>* v, const T* line, long long st
         const long long step = (long long)(2 * TL) * st;
 #pragma unroll
         for (int it = 0; it < 16; ++it, s += step) v[it] = mkc<T>(__ldg(s), __ldg(s + st));
+    }
+}
+
+// the staggered divergence of a projection step as the line values of the first
+// (contiguous, axis-1) pass: pairs (rhs_{2p}, rhs_{2p+1}) of line i = L.lb, p = bio + TL it
+template <typename T, int TL>
+__device__ __forceinline__ void load_divergence_pairs(cx<T>* v, const Producer& q, const LineInfo& L, int bio) {
+    if (!L.valid) {
+#pragma unroll
+        for (int it = 0; it < 16; ++it) v[it] = mkc<T>(0, 0);
+        return;
+    }
+    const int i = L.lb;
+    const int ip = (i + 1 == q.nx) ? 0 : i + 1;
+    const T* u0 = reinterpret_cast<const T*>(q.u) + (long long)i * q.us0;
+    const T* u1 = reinterpret_cast<const T*>(q.u) + (long long)ip * q.us0;
+    const T* w0 = reinterpret_cast<const T*>(q.w) + (long long)i * q.ws0;
+    const T sx = (T)q.sx, sz = (T)q.sz;
+#pragma unroll
+    for (int it = 0; it < 16; ++it) {
+        const int j = 2 * (bio + it * TL);
+        const int j2 = (q.w_periodic && j + 2 == q.nz) ? 0 : j + 2;
+        const T du0 = __ldg(u1 + (long long)j * q.us1) - __ldg(u0 + (long long)j * q.us1);
+        const T du1 = __ldg(u1 + (long long)(j + 1) * q.us1) - __ldg(u0 + (long long)(j + 1) * q.us1);
+        const T wa = __ldg(w0 + (long long)j * q.ws1), wb = __ldg(w0 + (long long)(j + 1) * q.ws1);
+        const T wc = __ldg(w0 + (long long)j2 * q.ws1);
+        v[it] = mkc<T>(du0 * sx + (wb - wa) * sz, du1 * sx + (wc - wb) * sz);
     }
 }
 
@@ -341,7 +368,8 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
     if (fwd_in && fkind_of<OP>(p) != FK_CFFT) {
         const int kind = fkind_of<OP>(p);
         if (!STRIDED) {
-            load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
+            if (p.prod.active) load_divergence_pairs<T, TL>(v, p.prod, Lio, bio);
+            else load_pairs<T, TL>(v, rline, st, Lio.valid, p.vec_in, bio);
             if (chk) {
 #pragma unroll
                 for (int it = 0; it < 16; ++it) bad |= !(finite_t(v[it].x) && finite_t(v[it].y));
@@ -1416,7 +1444,7 @@ inline FftKernelFn strided_fn() {
 }
 template <typename T, int L, int OPV>
 inline FftKernelFn spipe_fn(bool strided) {
-    if constexpr (opb(OPV) == OP_MID) return nullptr;   // the MID step is not pipelined
+    if constexpr (opb(OPV) == OP_MID || L < 9) return nullptr;   // the MID step is not pipelined; nor short lines
     else return strided ? (FftKernelFn)fft_pass_spipe<T, L, OPV> : (FftKernelFn) nullptr;
 }
 
@@ -1439,8 +1467,8 @@ inline FftKernelFn spipe_fn(bool strided) {
             case FK_DCT2: return strided_fn<T, L, mid_op(FK_DCT2)>();                        \
             case FK_DST2: return strided_fn<T, L, mid_op(FK_DST2)>();                        \
             case FK_RFFT: return strided_fn<T, L, mid_op(FK_RFFT)>();                        \
-            case FK_DCT1: return strided_fn<T, L, mid_op(FK_DCT1)>();                        \
-            case FK_DST1: return strided_fn<T, L, mid_op(FK_DST1)>();                        \
+            case FK_DCT1: case FK_DST1: /* regular grids: the runtime-kind MID (build time) */     \
+                return NAME##_one<L, OP_MID>(s, pipe);                                                \
             default: /* fp64 complex: the specialised build spills (c4 MID +7 %) */                  \
                 if constexpr (sizeof(T) == 8) return NAME##_one<L, OP_MID>(s, pipe);                  \
                 else return strided_fn<T, L, mid_op(FK_CFFT)>();                             \

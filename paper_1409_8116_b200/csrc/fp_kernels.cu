@@ -36,10 +36,82 @@
 namespace fpb {
 
 using FftKernelFn = void (*)(const FftPass);
-FftKernelFn pick_fft_d_lo(int logM, bool strided, int op, bool pipe, int kind);
-FftKernelFn pick_fft_d_hi(int logM, bool strided, int op, bool pipe, int kind);
-FftKernelFn pick_fft_f_lo(int logM, bool strided, int op, bool pipe, int kind);
-FftKernelFn pick_fft_f_hi(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l4(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l6(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l8(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l9(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l11(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_d_l12(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l4(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l6(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l8(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l9(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l11(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_fft_f_l12(int logM, bool strided, int op, bool pipe, int kind);
+
+// ----------------------------------------------------------------------------
+// projection step (flow.py:114-139): the divergence as a stand-alone rhs (used when
+// the first pass cannot produce it, e.g. a dense-engine z axis) and the corrector
+template <typename T>
+__global__ void __launch_bounds__(256) divergence_kernel(const Producer q, T* rhs) {
+    const long long total = (long long)q.nx * q.nz;
+    const T sx = (T)q.sx, sz = (T)q.sz;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += (long long)gridDim.x * 256) {
+        const int i = (int)(e / q.nz), j = (int)(e - (long long)i * q.nz);
+        const int ip = (i + 1 == q.nx) ? 0 : i + 1;
+        const int jp = (q.w_periodic && j + 1 == q.nz) ? 0 : j + 1;
+        const T* u = reinterpret_cast<const T*>(q.u);
+        const T* w = reinterpret_cast<const T*>(q.w);
+        const T du = __ldg(u + ip * q.us0 + j * q.us1) - __ldg(u + i * q.us0 + j * q.us1);
+        const T dw = __ldg(w + i * q.ws0 + jp * q.ws1) - __ldg(w + i * q.ws0 + j * q.ws1);
+        rhs[e] = du * sx + dw * sz;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) correct_kernel(const CorrectPass c) {
+    const int nwz = c.w_periodic ? c.nz : c.nz + 1;
+    const long long nu = (long long)c.nx * c.nz, nw = (long long)c.nx * nwz;
+    const T* phi = reinterpret_cast<const T*>(c.phi);
+    const T cx = (T)c.cx, cz = (T)c.cz;
+    for (long long e = blockIdx.x * 256LL + threadIdx.x; e < nu + nw; e += (long long)gridDim.x * 256) {
+        if (e < nu) {
+            const int i = (int)(e / c.nz), j = (int)(e - (long long)i * c.nz);
+            const int im = (i == 0) ? c.nx - 1 : i - 1;
+            const T ph = __ldg(phi + e);
+            reinterpret_cast<T*>(c.u_out)[e] =
+                __ldg(reinterpret_cast<const T*>(c.u_in) + e) - cx * (ph - __ldg(phi + (long long)im * c.nz + j));
+            if (c.p) reinterpret_cast<T*>(c.p)[e] += ph;
+        } else {
+            const long long f = e - nu;
+            const int i = (int)(f / nwz), j = (int)(f - (long long)i * nwz);
+            T g = 0;   // wall faces: zero gradient (Neumann pressure), w stays pinned
+            if (c.w_periodic) {
+                const int jm = (j == 0) ? c.nz - 1 : j - 1;
+                g = __ldg(phi + (long long)i * c.nz + j) - __ldg(phi + (long long)i * c.nz + jm);
+            } else if (j > 0 && j < c.nz) {
+                g = __ldg(phi + (long long)i * c.nz + j) - __ldg(phi + (long long)i * c.nz + j - 1);
+            }
+            reinterpret_cast<T*>(c.w_out)[f] = __ldg(reinterpret_cast<const T*>(c.w_in) + f) - cz * g;
+        }
+    }
+}
+
+cudaError_t launch_divergence(const Producer& q, void* rhs, bool f32, cudaStream_t st) {
+    long long blocks = ((long long)q.nx * q.nz + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (f32) divergence_kernel<float><<<(int)blocks, 256, 0, st>>>(q, (float*)rhs);
+    else divergence_kernel<double><<<(int)blocks, 256, 0, st>>>(q, (double*)rhs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_correct(const CorrectPass& c, bool f32, cudaStream_t st) {
+    long long blocks = ((long long)c.nx * (2LL * c.nz + 1) + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (f32) correct_kernel<float><<<(int)blocks, 256, 0, st>>>(c);
+    else correct_kernel<double><<<(int)blocks, 256, 0, st>>>(c);
+    return cudaGetLastError();
+}
 
 // ----------------------------------------------------------------------------
 // dense engine, long lines: the same product as a register-tiled GEMM.  The CTA
@@ -356,14 +428,20 @@ size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes) {
 template <typename T>
 static FftKernelFn pick_fft(int logM, bool strided, int op, bool pipe, int kind = -1) {
     // kind >= 0 selects the MID specialised on that line kind (strided, non-pipelined)
-    if (sizeof(T) == 8)
-        return logM <= 8 ? pick_fft_d_lo(logM, strided, op, pipe, kind) : pick_fft_d_hi(logM, strided, op, pipe, kind);
-    return logM <= 8 ? pick_fft_f_lo(logM, strided, op, pipe, kind) : pick_fft_f_hi(logM, strided, op, pipe, kind);
+    using PickFn = FftKernelFn (*)(int, bool, int, bool, int);
+    static const PickFn d[14] = {nullptr, nullptr, nullptr, nullptr, pick_fft_d_l4, pick_fft_d_l4, pick_fft_d_l6,
+                                 pick_fft_d_l6, pick_fft_d_l8, pick_fft_d_l9, pick_fft_d_l9, pick_fft_d_l11,
+                                 pick_fft_d_l12, pick_fft_d_l12};
+    static const PickFn f[14] = {nullptr, nullptr, nullptr, nullptr, pick_fft_f_l4, pick_fft_f_l4, pick_fft_f_l6,
+                                 pick_fft_f_l6, pick_fft_f_l8, pick_fft_f_l9, pick_fft_f_l9, pick_fft_f_l11,
+                                 pick_fft_f_l12, pick_fft_f_l12};
+    if (logM < 4 || logM > 13) return nullptr;
+    return (sizeof(T) == 8 ? d : f)[logM](logM, strided, op, pipe, kind);
 }
 
-// Opt in to the full 227 KB per CTA AND ask for the max-shared carveout: left to
-// itself the driver sizes the L1/shared split for ONE resident CTA of the
-// kernel's request, capping e.g. 70 KB tiles at 1 CTA/SM instead of 3.
+// Opt in to the full 227 KB per CTA.  The L1/shared carveout stays the driver's
+// choice: forcing max-shared (FP_CARVEOUT=100, experiments only) measured 33 %
+// slower on c3 -- the twiddle / eigenvalue tables live in L1.
 static cudaError_t allow_smem(const void* fn) {
     if (!fn) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -377,11 +455,11 @@ static cudaError_t set_smem_attr() {
     static bool done = false;
     if (done) return cudaSuccess;
     cudaError_t e;
-    for (int l = 4; l <= 12; ++l)
+    for (int l = 4; l <= 13; ++l)
         for (int s = 0; s < 2; ++s)
             for (int op = 0; op < 3; ++op)
                 for (int pp = 0; pp < 2; ++pp) {
-                    for (int kind = -1; kind < (op == OP_MID ? 6 : 0); ++kind) {
+                    for (int kind = -1; kind < (op == OP_MID ? 4 : 0); ++kind) {   // (kinds 4, 5 use the runtime MID)
                         if ((e = allow_smem((const void*)pick_fft<double>(l, s, op, pp, kind))) != cudaSuccess) return e;
                         if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp, kind))) != cudaSuccess) return e;
                     }
@@ -409,7 +487,7 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     // the first pass, and only when two tiles of the planned width fit (measured:
     // halving the width or pipelining the fp64-heavy MID step loses)
     static const int use_spipe = env_flag("FP_SPIPE", 1);
-    static const int spipe_min = env_flag("FP_SPIPE_MINLOG", 9);
+    static const int spipe_min = env_flag("FP_SPIPE_MINLOG", 9);   // (instantiated from 9 up)
     const bool cin = (p.op == OP_INV) ? (p.ikind == IK_ICFFT || p.ikind == IK_IRFFT) : (p.fkind == FK_CFFT);
     const int want = cin ? (f32 ? ET_C64 : ET_C128) : (f32 ? ET_F32 : ET_F64);
     const bool dst = (p.op != OP_INV && p.fkind == FK_DST2) || (p.op != OP_FWD && p.ikind == IK_DST3);

@@ -32,6 +32,8 @@ cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st);
 cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* out, int out_type, cudaStream_t st);
 size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
 int strided_line_stride(const FftPass& p, bool f32);
+cudaError_t launch_divergence(const Producer& q, void* rhs, bool f32, cudaStream_t st);
+cudaError_t launch_correct(const CorrectPass& c, bool f32, cudaStream_t st);
 }  // namespace fpb
 
 using namespace fpb;
@@ -262,23 +264,26 @@ fp_status validate(const fp_config* c) {
 
 // Which engine runs the transform along an axis, and its FFT length.
 // rfft: axis is the real-FFT periodic axis.  Returns M (0 = dense).
+// longest complex FFT line held in one tile (2^13: 139 KB of fp64 shared memory)
+const long long kFftMax = 8192;
+
 // complex FFT length of an axis on the FFT engine, 0 = dense engine
 int fft_length(int bc, int kind, long long n, bool rfft, bool regular_fft = true) {
     if (bc == FP_BC_PERIODIC) {
         const long long M = rfft ? ((n % 2 == 0) ? n / 2 : 0) : n;
-        if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+        if (M >= 16 && M <= kFftMax && is_pow2(M)) return (int)M;
         return 0;
     }
     if (kind != FP_GRID_STAGGERED) {
         // DCT-I (n = M + 1) / DST-I (n = M - 1) as the real FFT of the 2M-point extension
         if (!regular_fft) return 0;
         const long long M = bc == FP_BC_NEUMANN ? n - 1 : n + 1;
-        if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+        if (M >= 16 && M <= kFftMax && is_pow2(M)) return (int)M;
         return 0;
     }
     if (n % 2) return 0;
     const long long M = n / 2;
-    if (M >= 16 && M <= 4096 && is_pow2(M)) return (int)M;
+    if (M >= 16 && M <= kFftMax && is_pow2(M)) return (int)M;
     return 0;
 }
 
@@ -756,7 +761,8 @@ FP_API fp_status fp_solve(const fp_plan* P, const void* rhs, int rhs_dtype, cons
 static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
-                            void* const* pass_events, void* xbuf, int ph_lo, int ph_hi) {
+                            void* const* pass_events, void* xbuf, int ph_lo, int ph_hi,
+                            const Producer* prod = nullptr) {
     if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
     const bool need_rhs = ph_lo == 0, need_out = ph_hi == 2;
     if ((need_rhs && !rhs) || (need_out && !out)) return fail(FP_ERR_VALUE, "rhs/out is NULL");
@@ -798,6 +804,22 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
         rhs = rsb;
         rhs_dtype = plan_fp;
         for (int a = 0; a < 3; ++a) rs_s[a] = (a < d) ? (out_dense ? os_s[a] : dense_r[a]) : 0;
+    }
+    // projection step: the first pass produces its lines from the face velocities
+    // (contiguous real-kind FFT pass on the last axis); otherwise a stand-alone
+    // divergence kernel fills the (dense) real scratch and the solve reads that
+    bool prod_in_pass = false;
+    if (prod && ph_lo == 0) {
+        const PassT& F = P->passes[0];
+        prod_in_pass = F.engine == EN_FFT && F.fp.op == OP_FWD && F.fp.family == FAM_CONTIG && F.t == d - 1 &&
+                       (F.fp.fkind == FK_DCT2 || F.fp.fkind == FK_RFFT);
+        if (!prod_in_pass) {
+            cudaError_t e = launch_divergence(*prod, rsb, P->f32, (cudaStream_t)stream);
+            if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("divergence launch failed: ") + cudaGetErrorString(e));
+            rhs = rsb;
+            rhs_dtype = plan_fp;
+            for (int a = 0; a < 3; ++a) rs_s[a] = (a < d) ? (out_dense ? os_s[a] : dense_r[a]) : 0;
+        }
     }
     double* mean_ws = P->mean_fix ? (double*)((char*)workspace + need - mean_bytes(P)) : nullptr;
     const int plan_type = P->f32 ? ET_F32 : ET_F64;
@@ -869,6 +891,8 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
             p.g = g;
             p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
             p.s.dc_out = dev_info ? &dev_info->dc : nullptr;
+            p.prod.active = 0;
+            if (first && prod_in_pass) { p.prod = *prod; p.prod.active = 1; }
             const size_t rb = P->f32 ? 4 : 8;
             auto even_ok = [&](long long s, int ext) { return ext <= 1 || (s % 2) == 0; };
             p.vec_in = (p.family == FAM_CONTIG) && g.in_st == 1 && (g.in_type == plan_type) &&
@@ -931,6 +955,68 @@ FP_API fp_status fp_solve_phase(const fp_plan* P, int phase, const void* rhs, in
     if (phase < 0 || phase > 2) return fail(FP_ERR_VALUE, "phase must be 0 (forward), 1 (middle) or 2 (backward)");
     return solve_impl(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
                       dev_info, nullptr, nullptr, xbuf, phase, phase);
+}
+
+// ---- projection step of the 2D staggered-grid flow (flow.py:284-295) ----------
+static fp_status projection_geometry(const fp_plan* P, double* dx, double* dz, int* w_periodic) {
+    if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
+    if (P->nranks > 1) return fail(FP_ERR_UNSUPPORTED, "projection step: single-GPU plans only");
+    const fp_config& c = P->cfg;
+    const bool zp = c.bc[1] == FP_BC_PERIODIC, zw = c.bc[1] == FP_BC_NEUMANN && c.kind[1] == FP_GRID_STAGGERED;
+    if (c.ndim != 2 || c.bc[0] != FP_BC_PERIODIC || !(zp || zw))
+        return fail(FP_ERR_UNSUPPORTED, "projection step: needs the flow plan (x periodic; z periodic or staggered "
+                                        "Neumann walls), flow.py:241-250");
+    *dx = c.length[0] / (double)c.n[0];
+    *dz = c.length[1] / (double)c.n[1];
+    *w_periodic = zp ? 1 : 0;
+    return FP_OK;
+}
+
+FP_API fp_status fp_solve_divergence(const fp_plan* P, const void* u, const int64_t* u_strides, const void* w,
+                                     const int64_t* w_strides, double scale, void* phi, const int64_t* phi_strides,
+                                     void* workspace, size_t workspace_bytes, void* stream, fp_solve_info* dev_info) {
+    double dx, dz;
+    int wp;
+    fp_status st = projection_geometry(P, &dx, &dz, &wp);
+    if (st != FP_OK) return st;
+    if (!u || !w || !phi) return fail(FP_ERR_VALUE, "u/w/phi is NULL");
+    if (!(scale != 0.0) || !std::isfinite(scale)) return fail(FP_ERR_VALUE, "scale must be finite and non-zero");
+    Producer q{};
+    q.u = u;
+    q.w = w;
+    q.nx = (int)P->n[0];
+    q.nz = (int)P->n[1];
+    q.w_periodic = wp;
+    q.us0 = u_strides ? u_strides[0] : q.nz;
+    q.us1 = u_strides ? u_strides[1] : 1;
+    q.ws0 = w_strides ? w_strides[0] : (wp ? q.nz : q.nz + 1);
+    q.ws1 = w_strides ? w_strides[1] : 1;
+    if (q.us0 < 0 || q.us1 < 0 || q.ws0 < 0 || q.ws1 < 0) return fail(FP_ERR_VALUE, "negative strides are not supported");
+    q.sx = 1.0 / (dx * scale);
+    q.sz = 1.0 / (dz * scale);
+    q.active = 0;
+    return solve_impl(P, u, P->f32 ? FP_F32 : FP_F64, nullptr, phi, phi_strides, workspace, workspace_bytes, stream,
+                      dev_info, nullptr, nullptr, nullptr, 0, 2, &q);
+}
+
+FP_API fp_status fp_project_correct(const fp_plan* P, const void* phi, const void* u_star, const void* w_star,
+                                    void* u_out, void* w_out, void* p_inout, double scale, void* stream) {
+    double dx, dz;
+    int wp;
+    fp_status st = projection_geometry(P, &dx, &dz, &wp);
+    if (st != FP_OK) return st;
+    if (!phi || !u_star || !w_star || !u_out || !w_out) return fail(FP_ERR_VALUE, "NULL array");
+    DeviceGuard dg(P->device);
+    CorrectPass c{};
+    c.phi = phi; c.u_in = u_star; c.w_in = w_star; c.u_out = u_out; c.w_out = w_out; c.p = p_inout;
+    c.cx = scale / dx;
+    c.cz = scale / dz;
+    c.nx = (int)P->n[0];
+    c.nz = (int)P->n[1];
+    c.w_periodic = wp;
+    cudaError_t e = launch_correct(c, P->f32, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("corrector launch failed: ") + cudaGetErrorString(e));
+    return FP_OK;
 }
 
 FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_dist_info* info) {
@@ -1085,7 +1171,7 @@ FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int dev
     else if (kind == FP_DST2 || kind == FP_DST3 || kind == FP_DCT2 || kind == FP_DCT3) M = (n % 2 == 0) ? n / 2 : 0;
     else if (kind == FP_DCT1) M = n - 1;   // real FFT of the 2M-point even extension
     else if (kind == FP_DST1) M = n + 1;   // ... of the odd extension
-    T->fft = M >= 16 && M <= 4096 && is_pow2(M);
+    T->fft = M >= 16 && M <= kFftMax && is_pow2(M);
     fp_status st;
     if (T->fft) {
         T->M = (int)M;

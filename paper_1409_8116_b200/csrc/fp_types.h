@@ -67,6 +67,18 @@ struct Scaling {
     double* dc_out;             // raw null-mode coefficient sink (or nullptr)
 };
 
+// rhs producer of a 2D projection step (flow.py:114-122, 290): the first pass
+// computes  rhs[i][j] = ((u[i+1][j] - u[i][j]) / dx + (w[i][j+1] - w[i][j]) / dz) / scale
+// (i periodic along axis 0; w has nz + 1 faces with walls, nz when periodic in z)
+// from the face arrays while it loads its lines, instead of reading an rhs array
+struct Producer {
+    const void* u;              // x-faces (nx, nz), plan-typed
+    const void* w;              // z-faces (nx, nz) or (nx, nz + 1)
+    long long us0, us1, ws0, ws1;   // element strides
+    double sx, sz;              // 1 / (dx * scale), 1 / (dz * scale)
+    int nx, nz, w_periodic, active;
+};
+
 struct FftPass {
     int op, fkind, ikind, family;
     int n;                      // real line length (or complex length for CFFT)
@@ -84,6 +96,7 @@ struct FftPass {
     const void* ww;             // M+1 roots e^{-i pi k/(2n)} (DCT/DST)
     int* nonfinite;             // first pass only
     double out_mult;            // extra output scale (DFT 1/n in TransformPlan)
+    Producer prod;              // first pass of a fused projection step (active = 0 otherwise)
 };
 
 struct DensePass {
@@ -96,6 +109,20 @@ struct DensePass {
     const void* mat;            // [n_out][n_in] Real (R2R) or Real2 (others)
     int* nonfinite;
     double out_mult;
+};
+
+// the projection corrector (flow.py:125-139, 292-295):
+//   u -= scale * (phi[i][j] - phi[i-1][j]) / dx,  w -= scale * (phi[i][j] - phi[i][j-1]) / dz
+// (wall faces keep w), optionally p += phi; dense C-order (nx, nz) / (nx, nz[+1]) arrays
+struct CorrectPass {
+    const void* phi;
+    const void* u_in;
+    const void* w_in;
+    void* u_out;
+    void* w_out;
+    void* p;                    // nullable
+    double cx, cz;              // scale / dx, scale / dz
+    int nx, nz, w_periodic;
 };
 
 struct ScalePass {              // stand-alone eigenvalue scale (dense middle)

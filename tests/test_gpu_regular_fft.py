@@ -108,3 +108,30 @@ def test_transform_plan_dct1_dst1(kind, M, axis, torch_cuda, rng):
     want = orc.forward_1d(kind.value, x, axis=axis)
     got = fp.TransformPlan(kind, n, axis=axis).execute(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
     assert np.abs(got - want).max() <= 1e-13 * n * np.abs(x).max() * 4
+
+
+# -- the longest FFT lines: M = 8192 complex (periodic n = 8192, real lines n = 16384) --
+@pytest.mark.parametrize("axes,fft_axes", [
+    ([(8192, orc.TWO_PI, P), (64, orc.TWO_PI, P)], [0, 1]),                      # CFFT 8192 as the MID
+    ([(32, 1.0, N, orc.STAGGERED), (16384, 1.0, N, orc.STAGGERED)], [0, 1]),      # DCT-II n = 16384, contiguous
+    ([(16384, 1.0, D, orc.STAGGERED), (32, 1.0, D, orc.STAGGERED)], [0, 1]),      # DST-II 16384, strided MID
+    ([(32, orc.TWO_PI, P), (16384, orc.TWO_PI, P)], [0, 1]),                     # real FFT n = 16384
+    ([(8193, 1.0, N, R), (17, 1.0, N, R)], [0, 1]),                              # DCT-I, M = 8192
+])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_longest_fft_lines(axes, fft_axes, precision, torch_cuda, rng):
+    _solve_and_check(orc.Case(axes, orc.FD2 if axes[0][2] != P else orc.SPECTRAL, precision), rng, fft_axes)
+
+
+@pytest.mark.parametrize("kind,n", [(fp.TransformKind.DFT, 8192), (fp.TransformKind.IDFT, 8192),
+                                    (fp.TransformKind.DCT2, 16384), (fp.TransformKind.DST3, 16384)])
+@pytest.mark.parametrize("axis", [0, 1])
+def test_transform_plan_longest(kind, n, axis, torch_cuda, rng):
+    shape = [3, 4]
+    shape[axis] = n
+    x = rng.standard_normal(shape)
+    if kind.is_complex:
+        x = x + 1j * rng.standard_normal(shape)
+    want = orc.forward_1d(kind.value, x, axis=axis)
+    got = fp.TransformPlan(kind, n, axis=axis).execute(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    assert np.abs(got - want).max() <= 1e-13 * n * np.abs(x).max() * 4

@@ -137,3 +137,17 @@ def test_config_rhs_compatibility():
     case = orc.config_case("c4", 16)
     rhs = orc.config_rhs("c4", case)
     assert abs(rhs.sum()) <= 1e-9 * np.abs(rhs).sum()
+
+
+@pytest.mark.parametrize("name", ["periodic", "walls", "walls_dense"])
+def test_projection_oracle_matches_reference_flow(name):
+    # fixtures made by the reference flow module (tests/golden/make_projection_golden.py)
+    from pathlib import Path
+
+    z = np.load(Path(__file__).resolve().parent / "golden" / "projection_v1.npz")
+    nx, nz, lx, lz, walls, scale = z[f"{name}/meta"]
+    L = (lx, lz)
+    u, w, phi = orc.project_step(z[f"{name}/ustar"], z[f"{name}/wstar"], scale, L, bool(walls))
+    for got, key in ((u, "u"), (w, "w"), (phi, "phi")):
+        np.testing.assert_allclose(got, z[f"{name}/{key}"], rtol=0, atol=1e-13 * np.abs(z[f"{name}/{key}"]).max())
+    assert np.abs(orc.staggered_divergence(u, w, L, bool(walls))).max() <= 1e-10
