@@ -36,7 +36,7 @@ __all__ = [
     "PERIODIC", "DIRICHLET", "NEUMANN", "REGULAR", "STAGGERED", "SPECTRAL", "FD2",
     "Axis", "Case", "axis_dx", "axis_points", "eigenvalues", "pair", "backward_scale",
     "null_coeff", "forward_1d", "backward_1d", "naive_transform", "makhoul_dct2",
-    "makhoul_dct3", "r1_via_rfft", "r1_inverse_via_irfft", "staggered_divergence", "staggered_gradient",
+    "makhoul_dct3", "r1_via_rfft", "r1_inverse_via_irfft", "mr_factors", "mr_perm", "mr_fft", "mr_transform", "staggered_divergence", "staggered_gradient",
     "projection_case", "project_step", "solve", "laplacian", "dense_matrix", "dense_solve", "CONFIGS",
     "config_case", "config_rhs", "relative_l2",
 ]
@@ -257,6 +257,93 @@ def r1_inverse_via_irfft(X: np.ndarray, kind: str) -> np.ndarray:
     S = np.zeros(X.shape[:-1] + (M + 1,), dtype=complex)
     S[..., 1:M] = -1j * X
     return (np.fft.irfft(S, n=2 * M, axis=-1) * (2 * M))[..., 1:M]
+
+
+# -- the mixed-radix engine's recipes (fp_mr.cu), restated with numpy ---------------
+def mr_factors(N: int, max_prime: int = 61):
+    """Radices in stage order: 16, 8, 4, 2, then odd primes <= max_prime ([] if none fit)."""
+    f, m = [], N
+    for r in (16, 8, 4, 2):
+        while m % r == 0:
+            f.append(r)
+            m //= r
+    p = 3
+    while p <= max_prime and m > 1:
+        while m % p == 0:
+            f.append(p)
+            m //= p
+        p += 2
+    return f if m == 1 else []
+
+
+def mr_perm(N: int, fac) -> np.ndarray:
+    """Digit-reversed position of input index j for the in-place DIT over `fac`."""
+    j = np.arange(N)
+    pos = np.zeros(N, dtype=np.int64)
+    mult = N
+    for R in reversed(fac):
+        mult //= R
+        pos += (j % R) * mult
+        j = j // R
+    return pos
+
+
+def mr_fft(z: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """Unnormalised complex FFT of the last axis by the kernel's algorithm: scatter
+    into digit-reversed order, then in-place DIT stages (radix R, span L) with
+    butterflies over {b L R + k1 + r L} twiddled by W_{LR}^{r k1}."""
+    N = z.shape[-1]
+    fac = mr_factors(N)
+    if not fac:
+        raise ValueError(f"FFT length {N} has a prime factor above 61: no mixed-radix plan")
+    sgn = 1.0 if inverse else -1.0
+    root = np.exp(sgn * 2j * np.pi * np.arange(N) / N)
+    w = np.empty(z.shape, dtype=np.complex128)
+    w[..., mr_perm(N, fac)] = z
+    L = 1
+    for R in fac:
+        Lq = L * R
+        r = np.arange(R)
+        W = root[(np.outer(r, r) % R) * (N // R)]
+        k1 = np.arange(L)
+        tw = root[(np.outer(r, k1) * (N // Lq)) % N]                    # (R, L)
+        blk = w.reshape(z.shape[:-1] + (N // Lq, R, L)) * tw
+        w = np.einsum("kr,...brl->...bkl", W, blk).reshape(z.shape)
+        L = Lq
+    return w
+
+
+def mr_transform(kind: str, x: np.ndarray) -> np.ndarray:
+    """Unnormalised scipy-type transform of the last axis by the mixed-radix recipes
+    (any n: Makhoul for II/III, even/odd extensions for I, full complex FFTs)."""
+    n = x.shape[-1]
+    j = np.arange(n)
+    mk = np.where(j % 2 == 0, j // 2, n - 1 - j // 2)           # Makhoul position of x_j
+    if kind in ("dct2", "dst2"):
+        v = np.empty(x.shape, dtype=np.complex128)
+        v[..., mk] = x * ((-1.0) ** j if kind == "dst2" else 1.0)
+        V = mr_fft(v)
+        y = 2.0 * (np.exp(-1j * np.pi * j / (2 * n)) * V).real
+        return y[..., ::-1] if kind == "dst2" else y
+    if kind in ("dct3", "dst3"):
+        X = x[..., ::-1] if kind == "dst3" else x
+        Xn = np.concatenate([np.zeros(X.shape[:-1] + (1,)), X[..., :0:-1]], axis=-1)   # X_{n-k}, X_n = 0
+        W = np.exp(1j * np.pi * j / (2 * n)) * (X - 1j * Xn)
+        W[..., 0] = X[..., 0]
+        y = mr_fft(W, inverse=True)[..., mk].real
+        return y * (-1.0) ** j if kind == "dst3" else y
+    if kind == "dct1":
+        z = np.concatenate([x, x[..., -2:0:-1]], axis=-1)
+        return mr_fft(z.astype(np.complex128))[..., :n].real
+    if kind == "dst1":
+        zero = np.zeros(x.shape[:-1] + (1,))
+        z = np.concatenate([zero, x, zero, -x[..., ::-1]], axis=-1)
+        return -mr_fft(z.astype(np.complex128))[..., 1:n + 1].imag
+    if kind == "dft":
+        return mr_fft(x.astype(np.complex128)) / n
+    if kind == "idft":
+        return mr_fft(x.astype(np.complex128), inverse=True)
+    raise ValueError(kind)
 
 
 # -- flow.py: the projection step around the solve (SURVEY.md 8(f)2) ---------------

@@ -614,20 +614,6 @@ __device__ __forceinline__ cx<T> rsplit2(cx<T> zk, cx<T> zm, cx<T> tk) {
     return mkc<T>(A.x + tB.y, A.y - tB.x);
 }
 
-// cst / lam for modes off the null mode (lam < 0 strictly): no select needed
-template <typename T>
-__device__ __forceinline__ T eig_factor_nz(const Scaling& s, const LineInfo& L, int kt, double cst) {
-    // absent axes contribute +0.0 (exact), so the adds are unconditional and
-    // the sum keeps the reference's axis order ((l0 + l1) + l2)
-    const double lam = ((L.before + __ldg(&s.lam_t[kt])) + L.after1) + L.after2;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
-    double e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    return (T)(cst * r);
-}
 
 // ----------------------------------------------------------------------------
 // transform + post/mid/pre + store of one placed tile (contains barriers;

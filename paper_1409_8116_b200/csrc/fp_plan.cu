@@ -27,6 +27,8 @@
 namespace fpb {
 cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st);
 cudaError_t launch_dense_pass(const DensePass& p, bool f32, cudaStream_t st);
+cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st);
+size_t mr_smem_bytes(const MrPass& p, bool f32);
 cudaError_t launch_scale_pass(const ScalePass& p, bool f32, cudaStream_t st);
 cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st);
 cudaError_t launch_cast(const void* in, int in_type, const CastPass& p, void* out, int out_type, cudaStream_t st);
@@ -53,7 +55,7 @@ static fp_status fail(fp_status st, const std::string& msg) {
 namespace {
 
 enum Buf { B_RHS = 0, B_OUT = 1, B_RS = 2, B_CW = 3, B_X = 4 };  // B_X: caller's exchange buffer (distributed)
-enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2 };
+enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2, EN_MR = 3 };
 enum Layout { LY_REAL = 0, LY_CPLX = 1 };  // state of the data in the buffer
 
 struct DevTables {
@@ -64,6 +66,14 @@ struct DevTables {
     void* mat_b = nullptr;  // dense backward
     int fwd_nout = 0, fwd_nin = 0, bwd_nout = 0, bwd_nin = 0;
     bool fwd_cpx = false, bwd_cpx = false;
+    // mixed-radix engine (fp_mr.cu): one FFT length for both directions of a pair
+    bool mr = false;
+    int mrN = 0;
+    int fwd_kind = 0, bwd_kind = 0;
+    std::vector<int> fac;
+    void* mr_root = nullptr;
+    void* mr_wq = nullptr;
+    void* mr_perm = nullptr;
 };
 
 struct PassT {
@@ -74,6 +84,7 @@ struct PassT {
     int in_layout, out_layout;
     FftPass fp;
     DensePass dp;
+    MrPass mp;
     ScalePass sp;
     int a, b;            // other axes (-1 = dummy)
     bool dist_mid;       // MID over the all-to-all receive layout (blocked axis 0)
@@ -160,6 +171,14 @@ struct DeviceGuard {
 };
 
 bool is_pow2(long long x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    const int x = std::atoi(v);
+    return x > 0 ? x : dflt;
+}
+
 int ilog2(long long x) { int l = 0; while ((1LL << l) < x) ++l; return l; }
 
 // upload a long double table rounded to the plan precision (complex pairs or reals)
@@ -204,6 +223,112 @@ fp_status upload(AllocT& allocs, const std::vector<long double>& v, bool f32, vo
     }
     *out = d;
     return FP_OK;
+}
+
+template <typename AllocT>
+fp_status upload_ints(AllocT& allocs, const std::vector<int>& v, void** out) {
+    *out = nullptr;
+    void* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, v.size() * sizeof(int)));
+    allocs.push_back(d);
+    CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    *out = d;
+    return FP_OK;
+}
+
+// complex FFT length of a mixed-radix line of transform `kind` (FP_* id, or
+// MR_RFFT / MR_IRFFT); 0 if the length has no mixed-radix plan in this build
+long long mr_length(int kind, long long n, bool f32) {
+    static const bool on = [] { const char* v = std::getenv("FP_MR"); return !(v && *v == '0'); }();
+    if (!on || n < 16) return 0;   // short lines: the dense engine
+    long long N = n;
+    if (kind == FP_DCT1) N = 2 * (n - 1);
+    if (kind == FP_DST1) N = 2 * (n + 1);
+    if (mr_factors(N, kMrMaxPrime).empty()) return 0;
+    const size_t line = (size_t)(N + (N - 1) / 16 + 1) * (f32 ? 8 : 16);
+    if (line > 200 * 1024) return 0;
+    return N;
+}
+
+// does one line of the fused MID (tile + spectrum buffer) fit a CTA?
+bool mr_mid_fits(const DevTables& T, long long n, bool f32) {
+    MrPass p{};
+    p.kind = T.fwd_kind;
+    p.n = (int)n;
+    p.N = T.mrN;
+    p.lines = 1;
+    p.mid = 1;
+    return mr_smem_bytes(p, f32) <= 200 * 1024;
+}
+
+// upload the root / quarter-wave / permutation tables of a mixed-radix axis
+template <typename AllocT>
+fp_status mr_setup(AllocT& allocs, DevTables& T, int kind, long long n, bool f32) {
+    const long long N = mr_length(kind, n, f32);
+    if (N == 0) return FP_OK;
+    T.fac = mr_factors(N, kMrMaxPrime);
+    if ((int)T.fac.size() > kMrMaxStages) return FP_OK;
+    T.mrN = (int)N;
+    std::vector<long double> r;
+    root_table(N, N, r);
+    fp_status st;
+    if ((st = upload(allocs, r, f32, &T.mr_root)) != FP_OK) return st;
+    root_table(4 * n, n + 1, r);   // e^{-i pi k/(2n)}
+    if ((st = upload(allocs, r, f32, &T.mr_wq)) != FP_OK) return st;
+    if ((st = upload_ints(allocs, mr_perm((int)N, T.fac), &T.mr_perm)) != FP_OK) return st;
+    T.mr = true;
+    return FP_OK;
+}
+
+// a mixed-radix pass of transform `kind` over lines of length n (geometry filled at solve time)
+MrPass mr_pass(const DevTables& T, int kind, long long n, long long na, long long nb, bool f32, bool strided,
+               int mid_ikind = -1) {
+    MrPass p{};
+    p.kind = kind;
+    p.mid = mid_ikind >= 0;
+    p.ikind = p.mid ? mid_ikind : 0;
+    p.n = (int)n;
+    p.N = T.mrN;
+    p.inv = (kind == FP_IDFT || kind == FP_DCT3 || kind == FP_DST3 || kind == MR_IRFFT) ? 1 : 0;
+    p.cin = (kind == FP_DFT || kind == FP_IDFT || kind == MR_IRFFT) ? 1 : 0;
+    p.cout = (kind == FP_DFT || kind == FP_IDFT || kind == MR_RFFT) ? 1 : 0;
+    p.n_in = kind == MR_IRFFT ? (int)(n / 2 + 1) : (int)n;
+    p.n_out = kind == MR_RFFT ? (int)(n / 2 + 1) : (int)n;
+    if (p.mid) {
+        p.n_out = (int)n;   // the inverse of the pair writes n values (complex for IDFT)
+        p.cout = mid_ikind == FP_IDFT ? 1 : 0;
+    }
+    p.nf = (int)T.fac.size();
+    for (int q = 0; q < p.nf; ++q) p.fac[q] = T.fac[(size_t)q];
+    p.root = T.mr_root;
+    p.wq = T.mr_wq;
+    p.perm = (const int*)T.mr_perm;
+    p.out_mult = 1.0;
+    const long long nl = na * nb;
+    p.lines = 1;
+    p.log_lines = 0;
+    p.g.na = (int)na;
+    p.g.nb = (int)nb;
+    // lines per CTA: contiguous lines fill a 48 KB tile (several CTAs per SM);
+    // strided lines are adjacent columns, so the tile is widened towards
+    // FP_MR_STRIDED_BYTES row segments while 3 tiles still fit an SM (measured:
+    // 1000^3 156 ms at 16-B rows vs 187 ms at 64-B rows with one tile per SM)
+    static const int contig_kb = env_int("FP_MR_CONTIG_KB", 48);
+    static const int strided_bytes = env_int("FP_MR_STRIDED_BYTES", 128);
+    static const int strided_kb = env_int("FP_MR_STRIDED_KB", 72);
+    const int eb = (p.cin ? 2 : 1) * (f32 ? 4 : 8);
+    while (p.lines < 32 && p.lines < nl) {
+        MrPass q = p;
+        q.lines *= 2;
+        const size_t sm = mr_smem_bytes(q, f32);
+        const bool want = sm <= (size_t)contig_kb * 1024 ||
+                          (strided && p.lines * eb < strided_bytes && sm <= (size_t)strided_kb * 1024);
+        if (!want) break;
+        p = q;
+        p.log_lines += 1;
+    }
+    p.tiles = (int)((nl + p.lines - 1) / p.lines);
+    return p;
 }
 
 // forward/backward transform ids of a (bc, kind) row (transforms.py:99-125)
@@ -291,12 +416,6 @@ int fft_length(int bc, int kind, long long n, bool rfft, bool regular_fft = true
 // its matrix tile (complex fp64 fits up to 8695 points); the matrix is n^2 entries
 const long long kDenseMax = 8192;
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    if (!v || !*v) return dflt;
-    const int x = std::atoi(v);
-    return x > 0 ? x : dflt;
-}
 
 // choose the tile shape of an FFT pass
 void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long nb) {
@@ -490,16 +609,20 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             if ((st = upload(P->allocs, wt, P->f32, &T.wt)) != FP_OK) { delete P; return st; }
             if ((st = upload(P->allocs, ww, P->f32, &T.ww)) != FP_OK) { delete P; return st; }
         } else {
+            const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
+            const int bk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 101 : FP_IDFT) : bwd[a];
+            T.fwd_kind = fk;
+            T.bwd_kind = bk;
+            if ((st = mr_setup(P->allocs, T, fk, cfg->n[a], P->f32)) != FP_OK) { delete P; return st; }
+            if (T.mr) continue;
             if (cfg->n[a] > kDenseMax) {
                 delete P;
                 return fail(FP_ERR_UNSUPPORTED, "axis length " + std::to_string(cfg->n[a]) +
-                                                    " needs the dense engine, limited to n <= 8192 in this build");
+                                                    " has a prime factor above 61 and needs the dense engine, limited to n <= 8192 in this build");
             }
             std::vector<double> m;
             int no, ni;
             bool cpx;
-            const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
-            const int bk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 101 : FP_IDFT) : bwd[a];
             dense_matrix(fk, (int)cfg->n[a], m, &no, &ni, &cpx);
             T.fwd_nout = no; T.fwd_nin = ni; T.fwd_cpx = cpx;
             if ((st = upload(P->allocs, m, P->f32, &T.mat_f)) != FP_OK) { delete P; return st; }
@@ -579,8 +702,16 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         ps.in_layout = in_cpx ? LY_CPLX : LY_REAL;
         ps.out_layout = out_cpx ? LY_CPLX : LY_REAL;
         other_axes(t, &ps.a, &ps.b);
-        DensePass& p = ps.dp;
         const DevTables& T = P->tab[t];
+        if (T.mr) {
+            ps.engine = EN_MR;
+            const long long* ext = complex_state ? P->cext : P->n;
+            const long long na = ps.a >= 0 ? ext[ps.a] : 1;
+            const long long nb = ps.b >= 0 ? ext[ps.b] : 1;
+            ps.mp = mr_pass(T, forward ? T.fwd_kind : T.bwd_kind, cfg->n[t], na, nb, P->f32, t != d - 1);
+            return ps;
+        }
+        DensePass& p = ps.dp;
         p.n_in = forward ? T.fwd_nin : T.bwd_nin;
         p.n_out = forward ? T.fwd_nout : T.bwd_nout;
         p.mat = forward ? T.mat_f : T.mat_b;
@@ -648,6 +779,30 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             P->passes.push_back(mid);
         } else if (Mx[t] > 0) {
             P->passes.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
+        } else if (P->tab[t].mr && mr_mid_fits(P->tab[t], cfg->n[t], P->f32)) {
+            // mixed-radix MID: forward, eigenvalue scale, inverse on the tile
+            PassT ps{};
+            ps.engine = EN_MR;
+            ps.phase = 1;
+            ps.t = t;
+            ps.in_buf = cur;
+            ps.out_buf = dst;
+            ps.in_layout = ps.out_layout = complex_state ? LY_CPLX : LY_REAL;
+            other_axes(t, &ps.a, &ps.b);
+            const long long* ext = complex_state ? P->cext : P->n;
+            const long long na = ps.a >= 0 ? ext[ps.a] : 1;
+            const long long nb = ps.b >= 0 ? ext[ps.b] : 1;
+            const DevTables& T = P->tab[t];
+            ps.mp = mr_pass(T, T.fwd_kind, cfg->n[t], na, nb, P->f32, t != d - 1, T.bwd_kind);
+            Scaling& sc = ps.mp.s;
+            sc.lam_t = P->d_lam[t];
+            sc.lam_a = ps.a >= 0 ? P->d_lam[ps.a] : nullptr;
+            sc.lam_b = ps.b >= 0 ? P->d_lam[ps.b] : nullptr;
+            sc.pos_t = t; sc.pos_a = ps.a; sc.pos_b = ps.b;
+            sc.bscale = P->bscale;
+            sc.inv_np = inv_np;
+            sc.singular = P->singular;
+            P->passes.push_back(ps);
         } else if (!rf) {
             // dense forward, scale, dense inverse on the same buffer
             int work = cur;
@@ -902,6 +1057,13 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                         even_ok(g.out_sa, g.na) && even_ok(g.out_sb, g.nb) &&
                         ((uintptr_t)g.out % (2 * rb) == 0);
             e = launch_fft_pass(p, P->f32, st);
+        } else if (T.engine == EN_MR) {
+            MrPass p = T.mp;
+            g.na = p.g.na; g.nb = p.g.nb;
+            p.g = g;
+            p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
+            p.s.dc_out = dev_info ? &dev_info->dc : nullptr;
+            e = launch_mr_pass(p, P->f32, st);
         } else if (T.engine == EN_DENSE) {
             DensePass p = T.dp;
             g.na = p.g.na; g.nb = p.g.nb;
@@ -1182,7 +1344,9 @@ FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int dev
         if ((st = upload(T->allocs, wt, T->f32, &T->tab.wt)) != FP_OK) { delete T; return st; }
         if ((st = upload(T->allocs, ww, T->f32, &T->tab.ww)) != FP_OK) { delete T; return st; }
     } else {
-        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length needs the dense engine (n <= 8192)"); }
+        if ((st = mr_setup(T->allocs, T->tab, kind, n, T->f32)) != FP_OK) { delete T; return st; }
+        if (T->tab.mr) { *out = T; return FP_OK; }
+        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length has a prime factor above 61 and needs the dense engine (n <= 8192)"); }
         std::vector<double> m;
         int no, ni;
         bool cpx;
@@ -1253,6 +1417,12 @@ FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int
         p.nonfinite = nullptr;
         p.s = Scaling{};
         e = launch_fft_pass(p, T->f32, (cudaStream_t)stream);
+    } else if (T->tab.mr) {
+        MrPass p = mr_pass(T->tab, T->kind, T->n, g.na, g.nb, T->f32, g.in_st != 1);
+        p.g = g;
+        p.out_mult = om;
+        p.nonfinite = nullptr;
+        e = launch_mr_pass(p, T->f32, (cudaStream_t)stream);
     } else {
         DensePass p{};
         const bool in_c = in_dtype == FP_C128 || in_dtype == FP_C64;

@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 namespace fpb {
 
@@ -247,6 +248,41 @@ bool dense_matrix(int kind, int n, std::vector<double>& m, int* n_out, int* n_in
         }
     }
     return true;
+}
+
+std::vector<int> mr_factors(long long N, int max_prime) {
+    std::vector<int> f;
+    if (N < 2) return f;
+    long long m = N;
+    static const int maxp2 = [] { const char* v = std::getenv("FP_MR_MAXPOW2"); return (v && *v) ? std::atoi(v) : 16; }();
+    for (int r : {16, 8, 4, 2})
+        while (r <= maxp2 && m % r == 0) { f.push_back(r); m /= r; }
+    for (int p = 3; p <= max_prime && m > 1; p += 2)
+        while (m % p == 0) { f.push_back(p); m /= p; }
+    if (m != 1) f.clear();
+    return f;
+}
+
+// input index j = d_1 + R_1 (d_2 + R_2 (...)) is read by the last stage's
+// butterfly as sub-sequence j mod R_s: position (j mod R_s) * N / R_s + pos'(j / R_s)
+std::vector<int> mr_perm(int N, const std::vector<int>& fac) {
+    std::vector<int> p((size_t)N);
+    for (int j0 = 0; j0 < N; ++j0) {
+        int j = j0, pos = 0, mult = N;
+        for (int q = (int)fac.size() - 1; q >= 0; --q) {
+            const int R = fac[(size_t)q];
+            mult /= R;
+            pos += (j % R) * mult;
+            j /= R;
+        }
+        p[(size_t)j0] = pos;
+    }
+    return p;
+}
+
+void root_table(long long den, long long count, std::vector<long double>& out) {
+    out.assign(2 * (size_t)count, 0.0L);
+    for (long long k = 0; k < count; ++k) root(k, den, &out[2 * (size_t)k], &out[2 * (size_t)k + 1]);
 }
 
 }  // namespace fpb

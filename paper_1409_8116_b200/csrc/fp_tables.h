@@ -18,5 +18,12 @@ double axis_dx(const AxisSpec& a);
 std::vector<double> eigenvalue_table(const AxisSpec& a, int approx);
 // kind: FP_DFT..FP_DCT3, or 100 (real-input DFT half spectrum), 101 (half spectrum -> real)
 bool dense_matrix(int kind, int n, std::vector<double>& m, int* n_out, int* n_in, bool* cpx);
+// mixed-radix engine: radices of N (16, 8, 4, 2, then odd primes <= max_prime,
+// stage order); empty if N has a larger prime factor
+std::vector<int> mr_factors(long long N, int max_prime);
+// digit-reversed position of every input index for the in-place DIT over `fac`
+std::vector<int> mr_perm(int N, const std::vector<int>& fac);
+// roots e^{-2 pi i k/den}, k = 0..count-1, interleaved (re, im)
+void root_table(long long den, long long count, std::vector<long double>& out);
 
 }  // namespace fpb

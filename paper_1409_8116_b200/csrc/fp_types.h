@@ -111,6 +111,39 @@ struct DensePass {
     double out_mult;
 };
 
+// Mixed-radix engine (any n whose FFT length factors into primes <= 61): one
+// in-place decimation-in-time FFT of length N per line in shared memory, input
+// placed in mixed-radix digit-reversed order.  kind = public FP_* transform id,
+// or MR_RFFT / MR_IRFFT (real-input DFT -> half spectrum and back).
+//   DFT / IDFT / RFFT / IRFFT: N = n;  DCT2 / DST2 / DCT3 / DST3: N = n (Makhoul
+//   reordering + quarter-wave twiddle, any parity);  DCT1: N = 2(n-1) (even
+//   extension);  DST1: N = 2(n+1) (odd extension).
+constexpr int MR_RFFT = 100, MR_IRFFT = 101;
+constexpr int kMrMaxStages = 24;
+constexpr int kMrMaxPrime = 61;
+struct MrPass {
+    int kind;
+    int n;                      // line length
+    int n_in, n_out;            // elements read / written per line
+    int N;                      // complex FFT length
+    int inv;                    // FFT direction: 1 = e^{+2 pi i jk/N}
+    int cin, cout;              // complex operands
+    int nf;                     // stages
+    int fac[kMrMaxStages];      // radix per stage (stage 0 first)
+    int lines, log_lines;       // lines per CTA (power of two)
+    int tiles;
+    Geometry g;
+    const void* root;           // N roots e^{-2 pi i k/N} (plan precision, complex)
+    const void* wq;             // n+1 roots e^{-i pi k/(2n)} (II / III kinds)
+    const int* perm;            // digit-reversed position of input index j (N)
+    int* nonfinite;
+    double out_mult;
+    // MID (forward -> eigenvalue scale -> inverse on the tile): ikind = the
+    // pair's inverse transform; n_in follows kind, n_out follows ikind
+    int mid, ikind;
+    Scaling s;
+};
+
 // the projection corrector (flow.py:125-139, 292-295):
 //   u -= scale * (phi[i][j] - phi[i-1][j]) / dx,  w -= scale * (phi[i][j] - phi[i][j-1]) / dz
 // (wall faces keep w), optionally p += phi; dense C-order (nx, nz) / (nx, nz[+1]) arrays
