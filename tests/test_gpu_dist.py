@@ -66,6 +66,9 @@ SMALL = {
     "c5d": orc.Case([(64, orc.TWO_PI, orc.PERIODIC)] * 3, orc.SPECTRAL),
     "dst2d": orc.Case([(64, 1.0, orc.DIRICHLET, orc.STAGGERED), (48, 1.5, orc.DIRICHLET, orc.STAGGERED)], orc.FD2),
     "perx": orc.Case([(64, 2.0, orc.PERIODIC), (12, 1.0, orc.DIRICHLET, orc.REGULAR), (10, 1.0, orc.DIRICHLET, orc.REGULAR)], orc.FD2),
+    # local axes on the mixed-radix engine (non-power-of-two lengths)
+    "mrwall": orc.Case([(64, 1.0, orc.NEUMANN, orc.STAGGERED), (60, 1.0, orc.NEUMANN, orc.STAGGERED), (45, 2.0, orc.NEUMANN, orc.STAGGERED)], orc.FD2),
+    "mrper": orc.Case([(64, orc.TWO_PI, orc.PERIODIC), (48, orc.TWO_PI, orc.PERIODIC), (30, orc.TWO_PI, orc.PERIODIC)], orc.SPECTRAL),
 }
 
 
