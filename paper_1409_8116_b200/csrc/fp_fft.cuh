@@ -481,7 +481,7 @@ __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& 
 
 // store of an inverse-transformed tile (natural-order data in shared memory)
 template <typename T, int LOGM, bool STRIDED, int OP>
-__device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm) {
+__device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm, int bio_off = 0) {
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
     const int LS = line_stride<T, LOGM, STRIDED>(p);
@@ -490,7 +490,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
     const int Lc = p.lines, logL = p.logLines;
     const Geometry& g = p.g;
     const int lio = STRIDED ? (tid & (Lc - 1)) : (tid >> LOGTL);
-    const int bio = STRIDED ? (tid >> logL) : (tid & (TL - 1));
+    const int bio = (STRIDED ? (tid >> logL) : (tid & (TL - 1))) + bio_off;
     cx<T>* line_io = sm + lio * LS;
     const T* zr_io = reinterpret_cast<const T*>(line_io);
     const LineInfo Lio = linfo[lio];
@@ -1290,6 +1290,83 @@ template <typename T, int LOGM, bool STRIDED, int OP>
 __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
     fft_pass_tile<T, LOGM, STRIDED, OP>(p);
 }
+
+// Strided complex pass (MID, or forward / inverse complex FFT) whose I/O tile is
+// twice as wide as one compute pass: the loads and stores cover 2W lines (twice
+// the row segment: 64-B rows for fp32 2048-point lines instead of 32-B), the
+// transform runs on W lines at a time with all 512 threads.  (c5: the axis-0
+// MID at a 16.8 MB row stride is bound by DRAM transactions -- 16-B rows took
+// it from 50 to 97 ms, 64-B rows from 50 to 40 ms.)
+template <typename T, int LOGM, int OP>
+__global__ void __launch_bounds__(512) fft_pass_wide(const FftPass p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    using S = Shape<LOGM>;
+    constexpr int TL = S::TL, LOGTL = S::LOGTL;
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(smem_raw + linfo_bytes(p.lines));
+    setup_lines<true, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+    const int tid = threadIdx.x;
+    const int LS = line_stride<T, LOGM, true>(p);
+    const int lio = tid & (p.lines - 1);
+    const int bio = tid >> p.logLines;   // row blocks [0, TL/2) of the first half
+    const LineInfo Lio = linfo[lio];
+    cx<T>* line_io = sm + lio * LS;
+    bool bad = false;
+#pragma unroll 1
+    for (int f = 0; f < 2; ++f) bad |= place_tile<T, LOGM, true, OP>(p, Lio, line_io, bio + f * (TL / 2));
+    if (bad) *p.nonfinite = 1;
+    __syncthreads();
+    const void* __restrict__ W = p.wfft;
+    const int jt = tid & (TL - 1);
+#pragma unroll 1
+    for (int f = 0; f < 2; ++f) {
+        const int lf = (tid >> LOGTL) + f * (p.lines >> 1);
+        cx<T>* line_f = sm + lf * LS;
+        if constexpr (opb(OP) == OP_MID) {
+            const Scaling& Sc = p.s;
+            const double cst = Sc.bscale * Sc.inv_np;
+            const LineInfo L = linfo[lf];
+            const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+            cx<T> v[16];
+            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            if (jt == 0) {
+                if (cap) *Sc.dc_out = (double)v[0].x;
+                v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
+            } else {
+                v[0] = cscale<T>(v[0], eig_factor_nz<T>(Sc, L, jt, cst));
+            }
+#pragma unroll
+            for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
+            fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+        } else {
+            fft_tile<opb(OP) == OP_INV, T, LOGM>(line_f, jt, W);
+        }
+    }
+    if constexpr (opb(OP) == OP_FWD) {
+        // natural-order complex spectrum: row k = 16 b + i at 17 b + i
+        if (!Lio.valid) return;
+        const T om = (T)p.out_mult;
+        const long long os = p.g.out_st;
+#pragma unroll 1
+        for (int f = 0; f < 2; ++f) {
+            const int b = bio + f * (TL / 2);
+            cx<T>* po = reinterpret_cast<cx<T>*>(p.g.out) + Lio.out_off + (long long)(16 * b) * os;
+#pragma unroll
+            for (int it = 0; it < 16; ++it, po += os) *po = cscale<T>(line_io[17 * b + it], om);
+        }
+    } else {
+#pragma unroll 1
+        for (int f = 0; f < 2; ++f) compute_store_tail<T, LOGM, true, OP>(p, linfo, sm, f * (TL / 2));
+    }
+}
+#define FP_FFT_WIDE(NAME, T, L)                                                     \
+    namespace fpb {                                                                 \
+    FftKernelFn NAME(int op) {                                                      \
+        return op == OP_MID ? fft_pass_wide<T, L, mid_op(FK_CFFT)>                  \
+             : op == OP_FWD ? fft_pass_wide<T, L, OP_FWD> : fft_pass_wide<T, L, OP_INV>; \
+    }                                                                               \
+    }
 
 // Long fp32 strided forward / inverse lines: at <= 64 registers two 512-thread
 // CTAs fit per SM (70 would allow one).

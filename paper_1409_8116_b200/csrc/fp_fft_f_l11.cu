@@ -3,3 +3,4 @@
 #include "fp_fft.cuh"
 
 FP_FFT_PICK(pick_fft_f_l11, float, 11, 11)
+FP_FFT_WIDE(pick_wide_f_l11, float, 11)

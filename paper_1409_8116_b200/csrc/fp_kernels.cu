@@ -48,6 +48,12 @@ FftKernelFn pick_fft_f_l8(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_f_l9(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_f_l11(int logM, bool strided, int op, bool pipe, int kind);
 FftKernelFn pick_fft_f_l12(int logM, bool strided, int op, bool pipe, int kind);
+FftKernelFn pick_wide_f_l11(int op);
+FftKernelFn pick_wide_f_l12(int op);
+static FftKernelFn pick_wide(int logM, bool f32, int op) {
+    if (!f32) return nullptr;
+    return logM == 11 ? pick_wide_f_l11(op) : (logM == 12 ? pick_wide_f_l12(op) : nullptr);
+}
 
 // ----------------------------------------------------------------------------
 // projection step (flow.py:114-139): the divergence as a stand-alone rhs (used when
@@ -464,6 +470,9 @@ static cudaError_t set_smem_attr() {
                         if ((e = allow_smem((const void*)pick_fft<float>(l, s, op, pp, kind))) != cudaSuccess) return e;
                     }
                 }
+    for (int l = 11; l <= 12; ++l)
+        for (int op = 0; op < 3; ++op)
+            if ((e = allow_smem((const void*)pick_wide(l, true, op))) != cudaSuccess) return e;
     if ((e = allow_smem((const void*)dense_pass_kernel<double>)) != cudaSuccess) return e;
     if ((e = allow_smem((const void*)dense_pass_kernel<float>)) != cudaSuccess) return e;
     done = true;
@@ -493,7 +502,7 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
     const bool dst = (p.op != OP_INV && p.fkind == FK_DST2) || (p.op != OP_FWD && p.ikind == IK_DST3);
     const size_t psmem = 2 * linfo_bytes(p.lines) + 2 * (size_t)p.lines * p.ls * 2 * rb;
     const bool r1 = (p.op == OP_INV ? p.ikind : p.fkind) >= FK_DCT1;   // DCT-I / DST-I: own placement
-    if (use_spipe && strided && p.op != OP_MID && p.logM >= spipe_min && !dst && !r1 && p.nonfinite == nullptr &&
+    if (use_spipe && strided && p.op != OP_MID && p.sub != 2 && p.logM >= spipe_min && !dst && !r1 && p.nonfinite == nullptr &&
         p.g.in_type == want && psmem <= 227 * 1024) {
         FftKernelFn fn = f32 ? pick_fft<float>(p.logM, true, p.op, true) : pick_fft<double>(p.logM, true, p.op, true);
         int dev = 0, sms = 0, per_sm = 0;
@@ -515,6 +524,12 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
         }
     }
     const size_t smem = fft_pass_smem_bytes(p, rb);
+    if (p.sub == 2) {
+        FftKernelFn w = pick_wide(p.logM, f32, p.op);
+        if (!w || !strided) return cudaErrorInvalidValue;
+        w<<<p.tiles, threads / 2, smem, st>>>(p);
+        return cudaGetLastError();
+    }
     static const int mid_spec = env_flag("FP_MID_KIND_KERNELS", 1);   // 0: one MID kernel for all kinds (A/B)
     const int kind = (p.op == OP_MID && mid_spec) ? p.fkind : -1;
     FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false, kind)

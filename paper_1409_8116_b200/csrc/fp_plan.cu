@@ -451,6 +451,21 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
             p.logLines -= 1;
             p.ls = strided_line_stride(p, f32);
         }
+        // complex fp32 MID on 2048 / 4096-point lines: the 512-thread cap leaves
+        // 32-B (16-B) rows; a tile of twice the width runs as two compute halves
+        static const int mid_wide = env_int("FP_MID_WIDE", 1);
+        static const int io_wide = env_int("FP_IO_WIDE", 1);
+        const bool cfft = (p.op == OP_INV) ? p.ikind == IK_ICFFT : p.fkind == FK_CFFT;
+        const bool want_wide = (p.op == OP_MID) ? mid_wide == 1 : io_wide == 1;
+        p.sub = 1;
+        if (want_wide && f32 && in_cpx && cfft && (p.logM == 11 || p.logM == 12) &&
+            (p.lines << logTL) == 512 && p.lines * 2 <= nb && p.lines * 2 * eb <= strided_bytes) {
+            FftPass q = p;
+            q.lines *= 2;
+            q.logLines += 1;
+            q.ls = strided_line_stride(q, f32);
+            if (fft_pass_smem_bytes(q, real_bytes) <= 200 * 1024) { p = q; p.sub = 2; }
+        }
         p.nbt = (int)((nb + p.lines - 1) / p.lines);
         p.tiles = (int)(na * p.nbt);
     }

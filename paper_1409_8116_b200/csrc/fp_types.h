@@ -97,6 +97,8 @@ struct FftPass {
     int* nonfinite;             // first pass only
     double out_mult;            // extra output scale (DFT 1/n in TransformPlan)
     Producer prod;              // first pass of a fused projection step (active = 0 otherwise)
+    int sub;                    // STRIDED MID: compute sub-tiles per I/O tile (0/1 = one; 2 = the
+                                // tile is twice as wide as one 512-thread compute pass)
 };
 
 struct DensePass {
