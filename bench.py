@@ -372,17 +372,46 @@ def run_ours(args, ws, rank, local):
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for k in range(args.steps):
-        step(pass_events[k])
-    t_end.record(stream)
-    torch.cuda.synchronize(dev)
+    # small grids are launch-bound: one CUDA-graph replay per solve (SolverPlan.capture)
+    use_graph = n_pts <= (1 << 22)
+    if use_graph:
+        cap = plan.capture(rhs, out)
+        for _ in range(max(args.warmup, 1)):
+            cap.replay()
+        torch.cuda.synchronize(dev)
+        timed = cap.replay
+    else:
+        timed = step
+    l2_resident = n_pts * s < (128 << 20)
+    if l2_resident:
+        # the field fits L2: flush it (write 256 MiB) before every step and time
+        # each solve alone between its own events
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            timed()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        elapsed_ms = sum(a.elapsed_time(b) for a, b in evs)
+    else:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            timed()
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        elapsed_ms = t_start.elapsed_time(t_end)
     if dist is not None:
         dist.barrier()
     clocks = sampler.stop()
-    elapsed_ms = t_start.elapsed_time(t_end)
+    # per-kernel durations: a second pass of K solves with events between the kernels
+    # (kept out of the timed region: on 64^3 the event records cost more than a kernel)
+    for k in range(args.steps):
+        step(pass_events[k])
+    torch.cuda.synchronize(dev)
     if dist is not None:
         tt = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -441,7 +470,11 @@ def run_ours(args, ws, rank, local):
             "data": "synthetic (seeded N(0,1) field with its mean removed, generated on device)",
             "config": {"workload": WORKLOADS[args.config], "grid": list(shape),
                        "parallelism": "replicas" if ws > 1 else "single-gpu",
-                       "l2": "inputs (%.2f GiB/field) larger than L2; no flush" % (n_pts * s / 2**30)},
+                       "l2": ("inputs (%.2f GiB/field) larger than L2; no flush" % (n_pts * s / 2**30))
+                       if not l2_resident else
+                       "field (%.1f MiB) smaller than L2: 256 MiB flush before every step, each solve timed alone"
+                       % (n_pts * s / 2**20),
+                       "launch": "cuda-graph replay of one solve per step" if use_graph else "one fp_solve call per step"},
             "gpoints_per_s": value * n_pts / 1e9,
             "roofline": roofline,
             "cpu_baseline": cpu,
