@@ -451,6 +451,14 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
             p.logLines -= 1;
             p.ls = strided_line_stride(p, f32);
         }
+        // forward / inverse tiles: 256 threads while the rows stay >= 64 B (two
+        // resident tiles per SM beat 128-B rows at one: c4 y-rFFT 2.53 -> 2.16 ms)
+        static const int io_threads = env_int("FP_TILE_THREADS_STRIDED", 256);
+        while (p.op != OP_MID && p.lines > 1 && (p.lines << logTL) > io_threads && p.lines * eb > 64) {
+            p.lines /= 2;
+            p.logLines -= 1;
+            p.ls = strided_line_stride(p, f32);
+        }
         // complex fp32 MID on 2048 / 4096-point lines: the 512-thread cap leaves
         // 32-B (16-B) rows; a tile of twice the width runs as two compute halves
         static const int mid_wide = env_int("FP_MID_WIDE", 1);
