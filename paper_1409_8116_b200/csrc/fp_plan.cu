@@ -425,7 +425,7 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
     // FP_TILE_THREADS_CONTIG / FP_TILE_BYTES_STRIDED: tuning overrides (benchmarks only)
     static const int contig_threads = env_int("FP_TILE_THREADS_CONTIG", 32);
     static const int strided_bytes_io = env_int("FP_TILE_BYTES_STRIDED", 128);
-    static const int strided_bytes_mid = env_int("FP_TILE_BYTES_MID", 64);
+    static const int strided_bytes_mid = env_int("FP_TILE_BYTES_MID", 128);
     const int strided_bytes = p.op == OP_MID ? strided_bytes_mid : strided_bytes_io;
     if (p.family == FAM_CONTIG) {
         lines = std::max(1, contig_threads >> logTL);
@@ -451,10 +451,11 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
             p.logLines -= 1;
             p.ls = strided_line_stride(p, f32);
         }
-        // forward / inverse tiles: 256 threads while the rows stay >= 64 B (two
-        // resident tiles per SM beat 128-B rows at one: c4 y-rFFT 2.53 -> 2.16 ms)
+        // 256 threads while the rows stay >= 64 B (two resident tiles per SM beat
+        // 128-B rows at one: c4 y-rFFT 2.53 -> 2.16 ms, c4 MID 4.18 -> 3.74 ms;
+        // c3's real-line MID keeps 128-B rows at 256 threads: 0.729 -> 0.713 ms)
         static const int io_threads = env_int("FP_TILE_THREADS_STRIDED", 256);
-        while (p.op != OP_MID && p.lines > 1 && (p.lines << logTL) > io_threads && p.lines * eb > 64) {
+        while (p.lines > 1 && (p.lines << logTL) > io_threads && p.lines * eb > 64) {
             p.lines /= 2;
             p.logLines -= 1;
             p.ls = strided_line_stride(p, f32);
