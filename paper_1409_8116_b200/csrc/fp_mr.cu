@@ -343,9 +343,13 @@ __device__ __forceinline__ void mr_fft(const MrCtx<T>& c, const MrPass& p, bool 
 // forward axis): fill(kind) -> FFT -> emit into the spectrum buffer with the
 // eigenvalue factor (solver.py:216-223: null capture, bscale / lambda) ->
 // fill(ikind) from that buffer -> inverse-direction FFT -> emit(ikind).
-template <typename T>
+// KIND / IKIND: the pass's transform (and, for a MID, its inverse; -1 otherwise)
+// as compile-time constants, so every per-element recipe switch folds away;
+// operands are plan-typed (the solve casts a foreign-typed rhs first)
+template <typename T, int KIND, int IKIND>
 __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool MID = IKIND >= 0;
     const int N = p.N, n = p.n;
     const int LT = p.lines, logLT = p.log_lines;
     const int tid = threadIdx.x;
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
         const long long ia = L.valid ? gl / g.nb : 0, ib = L.valid ? gl % g.nb : 0;
         L.in_off = ia * g.in_sa + ib * g.in_sb;
         L.out_off = ia * g.out_sa + ib * g.out_sb;
-        if (p.mid) {
+        if (MID) {
             // eigenvalue partial sums in the reference's axis order (eigenvalues.py:104-108)
             const Scaling& Sc = p.s;
             const double la = Sc.lam_a ? Sc.lam_a[ia] : 0.0, lb = Sc.lam_b ? Sc.lam_b[ib] : 0.0;
@@ -390,27 +394,29 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
     // ---- fill from global memory
     int bad = 0;
     const bool lmin_in = g.in_st != 1, lmin_out = g.out_st != 1;
-    mr_fill<T, 8>(c, p.kind, lmin_in, p.n_in,
+    const T* __restrict__ in_r = reinterpret_cast<const T*>(g.in);
+    const cx<T>* __restrict__ in_c = reinterpret_cast<const cx<T>*>(g.in);
+    mr_fill<T, 8>(c, KIND, lmin_in, p.n_in,
         [&](int l, int j) {
             const LineInfo& Ln = lines[l];
-            return Ln.valid ? ld_real<T>(g.in, g.in_type, Ln.in_off + (long long)j * g.in_st) : (T)0;
+            return Ln.valid ? __ldg(in_r + Ln.in_off + (long long)j * g.in_st) : (T)0;
         },
         [&](int l, int j) {
             const LineInfo& Ln = lines[l];
-            return Ln.valid ? ld_cx<T>(g.in, g.in_type, Ln.in_off + (long long)j * g.in_st) : mkc<T>(0, 0);
+            return Ln.valid ? __ldg(in_c + Ln.in_off + (long long)j * g.in_st) : mkc<T>(0, 0);
         }, chk, bad);
     if (bad) *p.nonfinite = 1;
     __syncthreads();
-    mr_fft<T>(c, p, p.inv != 0);
+    mr_fft<T>(c, p, KIND == FP_IDFT || KIND == FP_DCT3 || KIND == FP_DST3 || KIND == MR_IRFFT);
 
-    if (p.mid) {
+    if constexpr (MID) {
         // ---- spectrum -> scaled spectrum buffer (physical spectral order)
-        const int sr = mr_spec_reals(p.kind, n);
+        const int sr = mr_spec_reals(KIND, n);
         const Scaling& Sc = p.s;
         const bool sing = Sc.singular && Sc.dc_out;
         const double cst = Sc.bscale * Sc.inv_np;
-        const int nspec = (p.kind == FP_DFT) ? n : (p.kind == MR_RFFT ? n / 2 + 1 : n);
-        mr_emit<T>(c, p.kind, false, nspec,
+        const int nspec = (KIND == FP_DFT) ? n : (KIND == MR_RFFT ? n / 2 + 1 : n);
+        mr_emit<T>(c, KIND, false, nspec,
             [&](int l, int k, T y) {
                 const LineInfo& Ln = lines[l];
                 if (k == 0 && sing && Ln.null_line) *Sc.dc_out = (double)y;
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
             });
         __syncthreads();
         // ---- inverse recipe from the spectrum buffer
-        const int ik = p.ikind;
+        constexpr int ik = IKIND;
         mr_fill<T, 1>(c, ik, false, (ik == MR_IRFFT) ? n / 2 + 1 : n,
             [&](int l, int j) { return spec[l * sr + j]; },
             [&](int l, int j) { return mkc<T>(spec[l * sr + 2 * j], spec[l * sr + 2 * j + 1]); }, false, bad);
@@ -435,14 +441,16 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
 
     // ---- store (output recipe of the pass's last transform)
     const T om = (T)p.out_mult;
-    mr_emit<T>(c, p.mid ? p.ikind : p.kind, lmin_out, p.n_out,
+    T* __restrict__ out_r = reinterpret_cast<T*>(g.out);
+    cx<T>* __restrict__ out_c = reinterpret_cast<cx<T>*>(g.out);
+    mr_emit<T>(c, MID ? IKIND : KIND, lmin_out, p.n_out,
         [&](int l, int k, T y) {
             const LineInfo& Ln = lines[l];
-            if (Ln.valid) st_real<T>(g.out, g.out_type, Ln.out_off + (long long)k * g.out_st, y * om);
+            if (Ln.valid) out_r[Ln.out_off + (long long)k * g.out_st] = y * om;
         },
         [&](int l, int k, cx<T> v) {
             const LineInfo& Ln = lines[l];
-            if (Ln.valid) st_cx<T>(g.out, g.out_type, Ln.out_off + (long long)k * g.out_st, cscale<T>(v, om));
+            if (Ln.valid) out_c[Ln.out_off + (long long)k * g.out_st] = cscale<T>(v, om);
         });
 }
 
@@ -450,18 +458,53 @@ size_t mr_smem_bytes(const MrPass& p, bool f32) {
     return mr_tile_bytes(p.lines, p.N, f32 ? 8 : 16) + mr_spec_bytes(p, f32 ? 4 : 8) + (size_t)p.lines * sizeof(LineInfo);
 }
 
-cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(mr_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(mr_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
+using MrKernelFn = void (*)(const MrPass);
+
+template <typename T>
+static MrKernelFn mr_pick(int kind, int ikind, bool mid) {
+    if (mid) {
+        switch (kind) {
+            case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, FP_DCT3>;
+            case FP_DST2: return mr_pass_kernel<T, FP_DST2, FP_DST3>;
+            case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, FP_DCT1>;
+            case FP_DST1: return mr_pass_kernel<T, FP_DST1, FP_DST1>;
+            case FP_DFT: return mr_pass_kernel<T, FP_DFT, FP_IDFT>;
+            case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, MR_IRFFT>;
+            default: return nullptr;
+        }
     }
-    const size_t smem = mr_smem_bytes(p, f32);
-    if (f32) mr_pass_kernel<float><<<p.tiles, 256, smem, st>>>(p);
-    else mr_pass_kernel<double><<<p.tiles, 256, smem, st>>>(p);
+    (void)ikind;
+    switch (kind) {
+        case FP_DFT: return mr_pass_kernel<T, FP_DFT, -1>;
+        case FP_IDFT: return mr_pass_kernel<T, FP_IDFT, -1>;
+        case FP_DST1: return mr_pass_kernel<T, FP_DST1, -1>;
+        case FP_DST2: return mr_pass_kernel<T, FP_DST2, -1>;
+        case FP_DST3: return mr_pass_kernel<T, FP_DST3, -1>;
+        case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, -1>;
+        case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, -1>;
+        case FP_DCT3: return mr_pass_kernel<T, FP_DCT3, -1>;
+        case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, -1>;
+        case MR_IRFFT: return mr_pass_kernel<T, MR_IRFFT, -1>;
+        default: return nullptr;
+    }
+}
+
+cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st) {
+    // operands must be plan-typed: real T, or complex T for the complex-side kinds
+    const int rt = f32 ? ET_F32 : ET_F64, ct = f32 ? ET_C64 : ET_C128;
+    const bool cin = p.cin != 0;
+    const bool cout = p.mid ? p.ikind == FP_IDFT : p.cout != 0;
+    if (p.g.in_type != (cin ? ct : rt) || p.g.out_type != (cout ? ct : rt)) return cudaErrorInvalidValue;
+    MrKernelFn fn = f32 ? mr_pick<float>(p.kind, p.ikind, p.mid != 0) : mr_pick<double>(p.kind, p.ikind, p.mid != 0);
+    if (!fn) return cudaErrorInvalidValue;
+    static bool attr[2][32] = {};
+    const int key = (p.mid ? 16 : 0) + (p.kind >= 100 ? 10 + p.kind - 100 : p.kind);
+    if (!attr[f32][key]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr[f32][key] = true;
+    }
+    fn<<<p.tiles, 256, mr_smem_bytes(p, f32), st>>>(p);
     return cudaGetLastError();
 }
 
