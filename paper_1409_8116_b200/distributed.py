@@ -176,3 +176,83 @@ class DistributedSolverPlan:
         rep = SolveReport(mode=self.config.mode, periodic_axes=self.config.periodic_axes)
         rep.removed_mean = (dc / self._np) / self._null if self.config.singular else 0.0
         return out_local, rep
+
+
+class MultiDeviceSolverPlan:
+    """Single-process multi-device solve of one global grid ("a
+    single-process multi-device wrapper").
+
+    One ``NativeBackend`` per device (rank r = ``devices[r]``, slab r of axis 0);
+    the two exchanges are device-to-device copies of the per-peer blocks (peer
+    copies over NVLink / NVSwitch when the devices differ) instead of NCCL.
+    ``solve(rhs)`` takes the whole field (numpy, or a tensor on any device) and
+    returns ``(solution, SolveReport)`` like ``SolverPlan.solve``: numpy in ->
+    numpy out, tensor in -> tensor on ``devices[0]``.  The same device may
+    appear several times (the ranks then share it; used by the tests).
+    """
+
+    def __init__(self, config: SolverConfig, devices):
+        t = dv.torch()
+        self.config = config
+        self.devices = [dv.require_cuda(d) for d in devices]
+        P = len(self.devices)
+        self.backends = [NativeBackend(config, P, r, self.devices[r]) for r in range(P)]
+        self.info = self.backends[0].info
+        self.a0 = int(self.info.local_n0)
+        from .solver import _ONES_NULL_COEFF
+        from .transforms import transform_pair_for
+        import math
+
+        pairs = [transform_pair_for(g.bc, g.kind) for g in config.grids]
+        self._np = math.prod(g.n for g in config.grids if g.bc.value == "periodic")
+        self._null = math.prod(_ONES_NULL_COEFF[p.forward](g.n) for g, p in zip(config.grids, pairs)) if config.singular else 1.0
+        self._t = t
+
+    def _sync(self):
+        for d in {(d.type, d.index): d for d in self.devices}.values():
+            self._t.cuda.synchronize(d)
+
+    def _exchange(self, src_attr, dst_attr):
+        """dst_r[s-th block] <- src_s[r-th block] for every rank pair (all-to-all by copies)."""
+        bes = self.backends
+        P = len(bes)
+        blk = getattr(bes[0], src_attr).numel() // P
+        self._sync()
+        for r in range(P):
+            dst = getattr(bes[r], dst_attr)
+            for s_ in range(P):
+                dst[s_ * blk:(s_ + 1) * blk].copy_(getattr(bes[s_], src_attr)[r * blk:(r + 1) * blk], non_blocking=True)
+        self._sync()
+
+    def solve(self, rhs):
+        t = self._t
+        host = not dv.is_tensor(rhs)
+        x = t.from_numpy(np.ascontiguousarray(rhs)) if host else rhs
+        if tuple(x.shape) != self.config.shape:
+            raise ValueError(f"rhs extents {tuple(x.shape)} do not match config extents {self.config.shape}")
+        bes, a0 = self.backends, self.a0
+        outs = []
+        for r, be in enumerate(bes):
+            slab = x[r * a0:(r + 1) * a0].to(be.device, non_blocking=False).contiguous()
+            out = be.new_output()
+            with t.cuda.device(be.device):
+                be.forward(slab, out)
+            outs.append(out)
+        self._exchange("send", "recv")
+        for be in bes:
+            with t.cuda.device(be.device):
+                be.middle()
+        self._exchange("recv", "send")
+        for r, be in enumerate(bes):
+            with t.cuda.device(be.device):
+                be.backward(outs[r])
+        self._sync()
+        status = [be.read_status().cpu() for be in bes]
+        dc = sum(float(s_[0]) for s_ in status)
+        if sum(float(s_[1]) for s_ in status) > 0:
+            raise ValueError("rhs contains non-finite values")
+        rep = SolveReport(mode=self.config.mode, periodic_axes=self.config.periodic_axes)
+        rep.removed_mean = (dc / self._np) / self._null if self.config.singular else 0.0
+        sol = t.cat([o.to(self.devices[0]) for o in outs], dim=0)
+        return (sol.cpu().numpy() if host else sol), rep
+

@@ -111,3 +111,24 @@ def test_dist_emulated_full_size(name, P, torch_cuda):
     err = (t.linalg.vector_norm(got - want) / t.linalg.vector_norm(want)).item()
     print(f"{name} P={P}: relative L2 vs single-GPU solve {err:.3e}")
     assert err <= 1e-12
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5d", "mrper"])
+def test_multi_device_wrapper_matches_single_gpu(name, P, torch_cuda, rng):
+    # the single-process multi-device wrapper; ranks share cuda:0 here
+    from paper_1409_8116_b200.distributed import MultiDeviceSolverPlan
+
+    case = SMALL[name]
+    config = _config(case)
+    rhs = rng.standard_normal(case.shape)
+    if case.singular:
+        rhs -= rhs.mean()
+    want, rep = fp.SolverPlan(config).solve(rhs)
+    plan = MultiDeviceSolverPlan(config, ["cuda:0"] * P)
+    got, rep2 = plan.solve(rhs)
+    assert isinstance(got, np.ndarray)
+    assert orc.relative_l2(got, want) <= 1e-12
+    assert rep2.removed_mean == pytest.approx(rep.removed_mean, abs=1e-12)
+    got_t, _ = plan.solve(torch_cuda.from_numpy(rhs).cuda())
+    assert orc.relative_l2(got_t.cpu().numpy(), want) <= 1e-12
