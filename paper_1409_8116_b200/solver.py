@@ -159,6 +159,17 @@ class _Events:
             pass
 
 
+class StridedAxisPass(tuple):
+    """(axis, shape): a transform pass along a non-contiguous axis, run in place
+    through strides (what the reference's ReorderPlan gathers into a line buffer)."""
+
+    def __new__(cls, axis, shape):
+        return tuple.__new__(cls, (int(axis), tuple(shape)))
+
+    axis = property(lambda s: s[0])
+    shape = property(lambda s: s[1])
+
+
 class SolverPlan:
     """Immutable plan for one configuration (solver.py:132-181), resident on one GPU.
 
@@ -219,6 +230,17 @@ class SolverPlan:
     @property
     def num_passes(self) -> int:
         return int(self._info.num_passes)
+
+    @property
+    def _reorder(self) -> dict:
+        """Axes the reference sends through its gather/scatter reorder seam
+        (solver.py:167-176: mixed plans, real axes other than the last).  Here
+        those lines are transformed in place through strides (strided tiles), so
+        each value only names that pass; the keys match the reference's."""
+        if self.mode != "mixed":
+            return {}
+        last = self.config.dims - 1
+        return {ax: StridedAxisPass(ax, self.shape) for ax in self._real_axes if ax != last}
 
     @property
     def _inv_lam(self) -> np.ndarray:

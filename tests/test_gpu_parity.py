@@ -360,3 +360,24 @@ def test_solve_batch_matches_individual_solves(torch_cuda, rng):
     bad[1][0, 0, 0] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
         plan.solve_batch(bad)
+
+
+def test_reorder_seam_keys_match_reference(torch_cuda, rng):
+    # tests/test_solver.py:291-320 assert these keys of plan._reorder; the GPU
+    # path transforms those axes in place through strides
+    BC, GK, AP = fp.BoundaryCondition, fp.GridKind, fp.Approximation
+    cfg = fp.SolverConfig((fp.GridSpec(6, 1.0, BC.PERIODIC), fp.GridSpec(5, 1.5, BC.NEUMANN, GK.STAGGERED),
+                           fp.GridSpec(4, 2.0, BC.NEUMANN, GK.STAGGERED)), AP.FINITE_DIFFERENCE_2)
+    plan = fp.SolverPlan(cfg)
+    assert 1 in plan._reorder and 2 not in plan._reorder
+    cfg2 = fp.SolverConfig((fp.GridSpec(5, 1.0, BC.DIRICHLET, GK.STAGGERED), fp.GridSpec(6, 2.0, BC.PERIODIC)),
+                           AP.FINITE_DIFFERENCE_2)
+    plan2 = fp.SolverPlan(cfg2)
+    assert plan2._reorder.keys() == {0}
+    rhs = rng.standard_normal((5, 6))
+    sol, rep = plan2.solve(rhs)
+    assert rep.periodic_axes == (1,)
+    want, _ = orc.solve(orc.Case([(5, 1.0, orc.DIRICHLET, orc.STAGGERED), (6, 2.0, orc.PERIODIC)], orc.FD2), rhs)
+    assert orc.relative_l2(sol, want) <= 1e-12
+    uniform = fp.SolverPlan(fp.SolverConfig((fp.GridSpec(8, 1.0, BC.NEUMANN, GK.STAGGERED),) * 2, AP.FINITE_DIFFERENCE_2))
+    assert uniform._reorder == {}
