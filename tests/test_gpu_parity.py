@@ -381,3 +381,26 @@ def test_reorder_seam_keys_match_reference(torch_cuda, rng):
     assert orc.relative_l2(sol, want) <= 1e-12
     uniform = fp.SolverPlan(fp.SolverConfig((fp.GridSpec(8, 1.0, BC.NEUMANN, GK.STAGGERED),) * 2, AP.FINITE_DIFFERENCE_2))
     assert uniform._reorder == {}
+
+
+@pytest.mark.parametrize("kind", [fp.TransformKind.DFT, fp.TransformKind.IDFT])
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_wide_strided_tiles_fp32_complex(kind, n, torch_cuda, rng):
+    # long complex fp32 lines on a strided axis run on the wide-tile kernel
+    # (I/O tile twice the 512-thread compute width); also through a solve (c5-like)
+    x = (rng.standard_normal((n, 3, 24)) + 1j * rng.standard_normal((n, 3, 24))).astype(np.complex64)
+    want = orc.forward_1d(kind.value, x.astype(np.complex128), axis=0)
+    got = fp.TransformPlan(kind, n, axis=0).execute(torch_cuda.from_numpy(x).cuda()).cpu().numpy()
+    assert np.abs(got - want).max() <= 2e-6 * np.log2(n) * np.abs(want).max()
+
+
+def test_wide_tiles_in_a_periodic_fp32_solve(torch_cuda, rng):
+    case = orc.Case([(2048, orc.TWO_PI, orc.PERIODIC), (2048, orc.TWO_PI, orc.PERIODIC), (16, orc.TWO_PI, orc.PERIODIC)],
+                    orc.SPECTRAL, "single")
+    grids = tuple(fp.GridSpec(a.n, a.length, fp.BoundaryCondition(a.bc), fp.GridKind(a.kind)) for a in case.axes)
+    plan = fp.SolverPlan(fp.SolverConfig(grids, fp.Approximation(case.approx), case.precision))
+    rhs = rng.standard_normal(case.shape).astype(np.float32)
+    rhs -= rhs.mean(dtype=np.float64)
+    got, rep = plan.solve(torch_cuda.from_numpy(rhs).cuda())
+    want, rm = orc.solve(case, rhs.astype(np.float64))
+    assert orc.relative_l2(got.cpu().numpy(), want) <= 1e-5
