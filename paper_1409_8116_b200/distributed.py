@@ -133,6 +133,15 @@ class DistributedSolverPlan:
         self.group = group
         self.nranks = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self._single = None
+        if self.nranks == 1 and backend is None:
+            # one rank: the whole grid is the slab; the single-GPU plan (fused MID, no exchange)
+            from .solver import SolverPlan
+
+            self._single = SolverPlan(config, device=device)
+            self.local_shape = tuple(config.shape)
+            self.local_slice = slice(0, config.shape[0])
+            return
         self.backend = backend if backend is not None else NativeBackend(config, self.nranks, self.rank, device)
         self.info = self.backend.info
         self.local_shape = tuple(self.backend.local_shape)
@@ -153,6 +162,9 @@ class DistributedSolverPlan:
 
         if tuple(rhs_local.shape) != self.local_shape:
             raise ValueError(f"local rhs extents {tuple(rhs_local.shape)} do not match {self.local_shape}")
+        if self._single is not None:
+            out_local, _, self._keep = self._single.solve_async(rhs_local, out_local)
+            return out_local
         if out_local is None:
             out_local = self.backend.new_output()
         be = self.backend
@@ -166,6 +178,8 @@ class DistributedSolverPlan:
     def solve(self, rhs_local, out_local=None):
         import torch.distributed as dist
 
+        if self._single is not None:
+            return self._single.solve(rhs_local, out_local)
         out_local = self.solve_async(rhs_local, out_local)
         be = self.backend
         status = be.read_status()

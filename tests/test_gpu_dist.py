@@ -132,3 +132,33 @@ def test_multi_device_wrapper_matches_single_gpu(name, P, torch_cuda, rng):
     assert rep2.removed_mean == pytest.approx(rep.removed_mean, abs=1e-12)
     got_t, _ = plan.solve(torch_cuda.from_numpy(rhs).cuda())
     assert orc.relative_l2(got_t.cpu().numpy(), want) <= 1e-12
+
+
+def test_distributed_plan_world_one_nccl(torch_cuda, rng):
+    # DistributedSolverPlan on a one-rank NCCL group: the whole grid is the slab
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_1409_8116_b200.distributed import DistributedSolverPlan
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0,
+                            device_id=torch_cuda.device("cuda", 0))
+    try:
+        case = SMALL["c4"]
+        config = _config(case)
+        rhs = rng.standard_normal(case.shape)
+        want, rep = fp.SolverPlan(config).solve(rhs)
+        plan = DistributedSolverPlan(config)
+        assert plan.local_shape == tuple(case.shape)
+        got, rep2 = plan.solve(torch_cuda.from_numpy(rhs).cuda())
+        assert orc.relative_l2(got.cpu().numpy(), want) <= 1e-12
+        assert rep2.removed_mean == pytest.approx(rep.removed_mean, abs=1e-12)
+        out = plan.solve_async(torch_cuda.from_numpy(rhs).cuda())
+        torch_cuda.cuda.synchronize()
+        assert orc.relative_l2(out.cpu().numpy(), want) <= 1e-12
+    finally:
+        dist.destroy_process_group()
