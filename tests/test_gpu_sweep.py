@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 ROWS = [(orc.PERIODIC, orc.REGULAR), (orc.DIRICHLET, orc.REGULAR), (orc.DIRICHLET, orc.STAGGERED),
         (orc.NEUMANN, orc.REGULAR), (orc.NEUMANN, orc.STAGGERED)]
 # FFT-engine lengths (powers of two, 2^k +- 1 for type I), mixed-radix, dense (primes > 61, short)
-LENGTHS = [2, 3, 5, 8, 12, 16, 17, 31, 32, 33, 45, 48, 60, 63, 64, 65, 67, 96, 100, 127, 128, 129, 150, 255, 256]
+LENGTHS = [1, 2, 3, 5, 8, 12, 16, 17, 31, 32, 33, 45, 48, 60, 63, 64, 65, 67, 96, 100, 127, 128, 129, 150, 255, 256]
 
 
 def random_case(r):
