@@ -448,7 +448,9 @@ def run_ours(args, ws, rank, local):
         "unit": "GB/s",
         "frac": pass_bytes / (avg_pass[top] * 1e-3) / 1e9 / hbm_peak,
         "traffic": traffic,
-        "kernel": f"pass {top} of {npass}",
+        "kernel": f"pass {top} of {npass}" + (
+            f" (MID: forward transform, eigenvalue divide, inverse transform along axis {int(plan._info.middle_axis)})"
+            if top == npass // 2 and npass % 2 == 1 else ""),
         "algorithmic_bytes_per_launch": pass_bytes,
         "peak_source": peak_src,
         "per_pass_ms": [round(float(x), 4) for x in avg_pass],
