@@ -30,6 +30,15 @@
 
 namespace fpb {
 
+// four reals fetched together (half-length inverse recipes)
+template <typename T> struct Quad { struct type { T x, y, z, w; }; };
+template <typename T>
+__device__ __forceinline__ typename Quad<T>::type make_double4_t(T a, T b, T c, T d) {
+    typename Quad<T>::type q;
+    q.x = a; q.y = b; q.z = c; q.w = d;
+    return q;
+}
+
 // Makhoul position of input index j (any n)
 __device__ __forceinline__ int mk_pos(int j, int n) { return (j & 1) ? n - 1 - (j >> 1) : (j >> 1); }
 
@@ -225,16 +234,72 @@ struct MrCtx {
     int slots, n, N, logLT;
     const int* __restrict__ perm;
     const cx<T>* __restrict__ wq;
+    const cx<T>* __restrict__ wt;   // half-length recipes: e^{-2 pi i k/n}, k <= n/2
 };
+
+// Half-length recipes for even n (HALF): the real line packed as z_m =
+// v_2m + i v_2m+1 (Makhoul order for DCT/DST, natural for the real FFT), one
+// complex FFT of length M = n/2, then the real-FFT untangle (rsplit) on the way
+// out -- and the inverse: tangle (rmerge), inverse FFT, de-interleave.  Same
+// identities as the FFT engine (oracle.makhoul_dct2 / makhoul_dct3); half the
+// shared-memory data and FFT work of the full-length recipes.
+template <typename T>
+__device__ __forceinline__ void put_half(cx<T>* z, const int* __restrict__ perm, int p, T x) {
+    reinterpret_cast<T*>(&z[P(__ldg(&perm[p >> 1]))])[p & 1] = x;
+}
+template <typename T>
+__device__ __forceinline__ T get_half(const cx<T>* z, int p) {
+    return reinterpret_cast<const T*>(&z[P(p >> 1)])[p & 1];
+}
 
 // placement of one line set: input recipe of transform `kind`, values from
 // getR(l, j) (real kinds) / getC(l, j) (complex); fetched in batches of U
-template <typename T, int U, typename GR, typename GC>
+template <typename T, int U, bool HALF, typename GR, typename GC>
 __device__ __forceinline__ void mr_fill(const MrCtx<T>& c, int kind, bool lminor, int nin, GR&& getR, GC&& getC,
                                         bool chk, int& bad) {
     cx<T>* const zall = c.zall;
     const int slots = c.slots, n = c.n, N = c.N;
     const int* __restrict__ perm = c.perm;
+    if constexpr (HALF) {
+        const int M = n >> 1;
+        if (kind == FP_DCT3 || kind == FP_DST3) {
+            // Z_k = rmerge(V_k, V_{M-k}, t_k), V_k = conj(w_k)(X'_k - i X'_{n-k}) (V_0 = X'_0), k < M
+            const bool dst = kind == FP_DST3;
+            auto xp = [&](int l, int k) { return getR(l, dst ? n - 1 - k : k); };   // X'_k, k < n
+            mr_walk_batched<U>(lminor, M, c.logLT, [&](int l, int k) {
+                // X'_k, X'_{n-k} (0 at k = 0), X'_{M-k}, X'_{M+k}
+                return make_double4_t<T>(xp(l, k), k > 0 ? xp(l, n - k) : (T)0, xp(l, M - k), xp(l, M + k));
+            }, [&](int l, int k, typename Quad<T>::type q) {
+                if (chk && !(finite_t(q.x) && finite_t(q.z))) bad = 1;
+                auto V = [&](int kk, T a, T b) -> cx<T> {
+                    if (kk == 0) return mkc<T>(a, 0);
+                    const cx<T> w = __ldg(&c.wq[kk]);
+                    return mkc<T>(w.x * a - w.y * b, -w.y * a - w.x * b);
+                };
+                const cx<T> vk = V(k, q.x, q.y), vm = V(M - k, q.z, q.w);
+                zall[l * slots + P(__ldg(&perm[k]))] = rmerge<T>(vk, vm, __ldg(&c.wt[k]));
+            });
+        } else if (kind == MR_IRFFT) {
+            mr_walk_batched<U>(lminor, M, c.logLT, [&](int l, int k) {
+                const cx<T> a = getC(l, k), b = getC(l, M - k);
+                return make_double4_t<T>(a.x, a.y, b.x, b.y);
+            }, [&](int l, int k, typename Quad<T>::type q) {
+                if (chk && !(finite_t(q.x) && finite_t(q.y) && finite_t(q.z) && finite_t(q.w))) bad = 1;
+                // the DC / Nyquist imaginary parts do not enter a real inverse (dense kind 101)
+                const cx<T> xk = mkc<T>(q.x, k == 0 ? (T)0 : q.y), xm = mkc<T>(q.z, k == 0 ? (T)0 : q.w);
+                zall[l * slots + P(__ldg(&perm[k]))] = rmerge<T>(xk, xm, __ldg(&c.wt[k]));
+            });
+        } else {
+            // DCT-II / DST-II (Makhoul packing) and the real FFT (natural packing)
+            mr_walk_batched<U>(lminor, n, c.logLT, [&](int l, int j) { return getR(l, j); }, [&](int l, int j, T x) {
+                if (chk && !finite_t(x)) bad = 1;
+                cx<T>* z = zall + l * slots;
+                if (kind == MR_RFFT) put_half<T>(z, perm, j, x);
+                else put_half<T>(z, perm, mk_pos(j, n), (kind == FP_DST2 && (j & 1)) ? -x : x);
+            });
+        }
+        return;
+    }
     if (kind == FP_DCT3 || kind == FP_DST3) {
         // W_k = conj(w_k) (X'_k - i X'_{n-k}), X' = X (DCT-III) or reverse(X) (DST-III), X'_n = 0
         const bool dst = kind == FP_DST3;
@@ -286,9 +351,39 @@ __device__ __forceinline__ void mr_fill(const MrCtx<T>& c, int kind, bool lminor
 }
 
 // output recipe of transform `kind`: putR(l, k, y) / putC(l, k, v) per output
-template <typename T, typename PR, typename PC>
+template <typename T, bool HALF, typename PR, typename PC>
 __device__ __forceinline__ void mr_emit(const MrCtx<T>& c, int kind, bool lminor, int nout, PR&& putR, PC&& putC) {
     const int slots = c.slots, n = c.n;
+    if constexpr (HALF) {
+        const int M = n >> 1;
+        mr_walk(lminor, nout, c.logLT, [&](int l, int k) {
+            const cx<T>* z = c.zall + l * slots;
+            if (kind == MR_RFFT || kind == FP_DCT2 || kind == FP_DST2) {
+                // untangle: V_q = rsplit(Z_q, Z_{M-q}, t_q), q <= M
+                int q = k;
+                bool hi = false;
+                if (kind != MR_RFFT) {
+                    const int kk = kind == FP_DST2 ? n - 1 - k : k;
+                    hi = kk > M;
+                    q = hi ? n - kk : kk;
+                }
+                const cx<T> V = rsplit<T>(z[P(q == M ? 0 : q)], z[P(q == 0 ? 0 : M - q)], __ldg(&c.wt[q]));
+                if (kind == MR_RFFT) { putC(l, k, V); return; }
+                const cx<T> U = cmul<T>(__ldg(&c.wq[q]), V);
+                putR(l, k, hi ? (T)-2 * U.y : (T)2 * U.x);
+                return;
+            }
+            // inverse kinds: de-interleave (Makhoul order for DCT-III / DST-III)
+            T y;
+            if (kind == MR_IRFFT) y = get_half<T>(z, k);
+            else {
+                y = get_half<T>(z, mk_pos(k, n));
+                if (kind == FP_DST3 && (k & 1)) y = -y;
+            }
+            putR(l, k, y);
+        });
+        return;
+    }
     const bool cout = kind == FP_DFT || kind == FP_IDFT || kind == MR_RFFT;
     mr_walk(lminor, nout, c.logLT, [&](int l, int k) {
         const cx<T>* z = c.zall + l * slots;
@@ -346,7 +441,7 @@ __device__ __forceinline__ void mr_fft(const MrCtx<T>& c, const MrPass& p, bool 
 // KIND / IKIND: the pass's transform (and, for a MID, its inverse; -1 otherwise)
 // as compile-time constants, so every per-element recipe switch folds away;
 // operands are plan-typed (the solve casts a foreign-typed rhs first)
-template <typename T, int KIND, int IKIND>
+template <typename T, int KIND, int IKIND, bool HALF>
 __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool MID = IKIND >= 0;
@@ -361,6 +456,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
     c.logLT = logLT;
     c.perm = p.perm;
     c.wq = reinterpret_cast<const cx<T>*>(p.wq);
+    c.wt = reinterpret_cast<const cx<T>*>(p.wt);
     const size_t tb = mr_tile_bytes(LT, N, sizeof(cx<T>));
     T* spec = reinterpret_cast<T*>(smem_raw + tb);
     LineInfo* lines = reinterpret_cast<LineInfo*>(smem_raw + tb + mr_spec_bytes(p, sizeof(T)));
@@ -396,7 +492,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
     const bool lmin_in = g.in_st != 1, lmin_out = g.out_st != 1;
     const T* __restrict__ in_r = reinterpret_cast<const T*>(g.in);
     const cx<T>* __restrict__ in_c = reinterpret_cast<const cx<T>*>(g.in);
-    mr_fill<T, 8>(c, KIND, lmin_in, p.n_in,
+    mr_fill<T, 8, HALF>(c, KIND, lmin_in, p.n_in,
         [&](int l, int j) {
             const LineInfo& Ln = lines[l];
             return Ln.valid ? __ldg(in_r + Ln.in_off + (long long)j * g.in_st) : (T)0;
@@ -416,7 +512,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
         const bool sing = Sc.singular && Sc.dc_out;
         const double cst = Sc.bscale * Sc.inv_np;
         const int nspec = (KIND == FP_DFT) ? n : (KIND == MR_RFFT ? n / 2 + 1 : n);
-        mr_emit<T>(c, KIND, false, nspec,
+        mr_emit<T, HALF>(c, KIND, false, nspec,
             [&](int l, int k, T y) {
                 const LineInfo& Ln = lines[l];
                 if (k == 0 && sing && Ln.null_line) *Sc.dc_out = (double)y;
@@ -432,7 +528,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
         __syncthreads();
         // ---- inverse recipe from the spectrum buffer
         constexpr int ik = IKIND;
-        mr_fill<T, 1>(c, ik, false, (ik == MR_IRFFT) ? n / 2 + 1 : n,
+        mr_fill<T, 1, HALF>(c, ik, false, (ik == MR_IRFFT) ? n / 2 + 1 : n,
             [&](int l, int j) { return spec[l * sr + j]; },
             [&](int l, int j) { return mkc<T>(spec[l * sr + 2 * j], spec[l * sr + 2 * j + 1]); }, false, bad);
         __syncthreads();
@@ -443,7 +539,7 @@ __global__ void __launch_bounds__(256, FP_MR_MINB) mr_pass_kernel(const MrPass p
     const T om = (T)p.out_mult;
     T* __restrict__ out_r = reinterpret_cast<T*>(g.out);
     cx<T>* __restrict__ out_c = reinterpret_cast<cx<T>*>(g.out);
-    mr_emit<T>(c, MID ? IKIND : KIND, lmin_out, p.n_out,
+    mr_emit<T, HALF>(c, MID ? IKIND : KIND, lmin_out, p.n_out,
         [&](int l, int k, T y) {
             const LineInfo& Ln = lines[l];
             if (Ln.valid) out_r[Ln.out_off + (long long)k * g.out_st] = y * om;
@@ -460,33 +556,48 @@ size_t mr_smem_bytes(const MrPass& p, bool f32) {
 
 using MrKernelFn = void (*)(const MrPass);
 
-template <typename T>
-static MrKernelFn mr_pick(int kind, int ikind, bool mid) {
+template <typename T, bool H>
+static MrKernelFn mr_pick_h(int kind, bool mid) {
     if (mid) {
         switch (kind) {
-            case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, FP_DCT3>;
-            case FP_DST2: return mr_pass_kernel<T, FP_DST2, FP_DST3>;
-            case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, FP_DCT1>;
-            case FP_DST1: return mr_pass_kernel<T, FP_DST1, FP_DST1>;
-            case FP_DFT: return mr_pass_kernel<T, FP_DFT, FP_IDFT>;
-            case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, MR_IRFFT>;
-            default: return nullptr;
+            case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, FP_DCT3, H>;
+            case FP_DST2: return mr_pass_kernel<T, FP_DST2, FP_DST3, H>;
+            case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, MR_IRFFT, H>;
+            default: break;
+        }
+        if constexpr (!H) {
+            switch (kind) {
+                case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, FP_DCT1, false>;
+                case FP_DST1: return mr_pass_kernel<T, FP_DST1, FP_DST1, false>;
+                case FP_DFT: return mr_pass_kernel<T, FP_DFT, FP_IDFT, false>;
+                default: break;
+            }
+        }
+        return nullptr;
+    }
+    switch (kind) {
+        case FP_DST2: return mr_pass_kernel<T, FP_DST2, -1, H>;
+        case FP_DST3: return mr_pass_kernel<T, FP_DST3, -1, H>;
+        case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, -1, H>;
+        case FP_DCT3: return mr_pass_kernel<T, FP_DCT3, -1, H>;
+        case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, -1, H>;
+        case MR_IRFFT: return mr_pass_kernel<T, MR_IRFFT, -1, H>;
+        default: break;
+    }
+    if constexpr (!H) {
+        switch (kind) {
+            case FP_DFT: return mr_pass_kernel<T, FP_DFT, -1, false>;
+            case FP_IDFT: return mr_pass_kernel<T, FP_IDFT, -1, false>;
+            case FP_DST1: return mr_pass_kernel<T, FP_DST1, -1, false>;
+            case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, -1, false>;
+            default: break;
         }
     }
-    (void)ikind;
-    switch (kind) {
-        case FP_DFT: return mr_pass_kernel<T, FP_DFT, -1>;
-        case FP_IDFT: return mr_pass_kernel<T, FP_IDFT, -1>;
-        case FP_DST1: return mr_pass_kernel<T, FP_DST1, -1>;
-        case FP_DST2: return mr_pass_kernel<T, FP_DST2, -1>;
-        case FP_DST3: return mr_pass_kernel<T, FP_DST3, -1>;
-        case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, -1>;
-        case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, -1>;
-        case FP_DCT3: return mr_pass_kernel<T, FP_DCT3, -1>;
-        case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, -1>;
-        case MR_IRFFT: return mr_pass_kernel<T, MR_IRFFT, -1>;
-        default: return nullptr;
-    }
+    return nullptr;
+}
+template <typename T>
+static MrKernelFn mr_pick(int kind, bool mid, bool half) {
+    return half ? mr_pick_h<T, true>(kind, mid) : mr_pick_h<T, false>(kind, mid);
 }
 
 cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st) {
@@ -495,10 +606,10 @@ cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st) {
     const bool cin = p.cin != 0;
     const bool cout = p.mid ? p.ikind == FP_IDFT : p.cout != 0;
     if (p.g.in_type != (cin ? ct : rt) || p.g.out_type != (cout ? ct : rt)) return cudaErrorInvalidValue;
-    MrKernelFn fn = f32 ? mr_pick<float>(p.kind, p.ikind, p.mid != 0) : mr_pick<double>(p.kind, p.ikind, p.mid != 0);
+    MrKernelFn fn = f32 ? mr_pick<float>(p.kind, p.mid != 0, p.half != 0) : mr_pick<double>(p.kind, p.mid != 0, p.half != 0);
     if (!fn) return cudaErrorInvalidValue;
-    static bool attr[2][32] = {};
-    const int key = (p.mid ? 16 : 0) + (p.kind >= 100 ? 10 + p.kind - 100 : p.kind);
+    static bool attr[2][64] = {};
+    const int key = (p.half ? 32 : 0) + (p.mid ? 16 : 0) + (p.kind >= 100 ? 10 + p.kind - 100 : p.kind);
     if (!attr[f32][key]) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;

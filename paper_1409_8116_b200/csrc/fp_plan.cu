@@ -69,6 +69,8 @@ struct DevTables {
     // mixed-radix engine (fp_mr.cu): one FFT length for both directions of a pair
     bool mr = false;
     int mrN = 0;
+    bool mr_half = false;   // half-length recipes (even n, II/III kinds and the real FFT)
+    void* mr_wt = nullptr;
     int fwd_kind = 0, bwd_kind = 0;
     std::vector<int> fac;
     void* mr_root = nullptr;
@@ -238,10 +240,18 @@ fp_status upload_ints(AllocT& allocs, const std::vector<int>& v, void** out) {
 
 // complex FFT length of a mixed-radix line of transform `kind` (FP_* id, or
 // MR_RFFT / MR_IRFFT); 0 if the length has no mixed-radix plan in this build
+bool mr_half_kind(int kind, long long n) {
+    static const bool on = [] { const char* v = std::getenv("FP_MR_HALF"); return !(v && *v == '0'); }();
+    const bool k2 = kind == FP_DCT2 || kind == FP_DST2 || kind == FP_DCT3 || kind == FP_DST3 ||
+                    kind == MR_RFFT || kind == MR_IRFFT;
+    return on && k2 && n % 2 == 0 && n / 2 >= 8 && !mr_factors(n / 2, kMrMaxPrime).empty();
+}
+
 long long mr_length(int kind, long long n, bool f32) {
     static const bool on = [] { const char* v = std::getenv("FP_MR"); return !(v && *v == '0'); }();
     if (!on || n < 16) return 0;   // short lines: the dense engine
     long long N = n;
+    if (mr_half_kind(kind, n)) N = n / 2;
     if (kind == FP_DCT1) N = 2 * (n - 1);
     if (kind == FP_DST1) N = 2 * (n + 1);
     if (mr_factors(N, kMrMaxPrime).empty()) return 0;
@@ -258,6 +268,7 @@ bool mr_mid_fits(const DevTables& T, long long n, bool f32) {
     p.N = T.mrN;
     p.lines = 1;
     p.mid = 1;
+    p.half = T.mr_half ? 1 : 0;
     return mr_smem_bytes(p, f32) <= 200 * 1024;
 }
 
@@ -269,12 +280,17 @@ fp_status mr_setup(AllocT& allocs, DevTables& T, int kind, long long n, bool f32
     T.fac = mr_factors(N, kMrMaxPrime);
     if ((int)T.fac.size() > kMrMaxStages) return FP_OK;
     T.mrN = (int)N;
+    T.mr_half = mr_half_kind(kind, n);
     std::vector<long double> r;
     root_table(N, N, r);
     fp_status st;
     if ((st = upload(allocs, r, f32, &T.mr_root)) != FP_OK) return st;
     root_table(4 * n, n + 1, r);   // e^{-i pi k/(2n)}
     if ((st = upload(allocs, r, f32, &T.mr_wq)) != FP_OK) return st;
+    if (T.mr_half) {
+        root_table(n, n / 2 + 1, r);   // e^{-2 pi i k/n}
+        if ((st = upload(allocs, r, f32, &T.mr_wt)) != FP_OK) return st;
+    }
     if ((st = upload_ints(allocs, mr_perm((int)N, T.fac), &T.mr_perm)) != FP_OK) return st;
     T.mr = true;
     return FP_OK;
@@ -302,6 +318,8 @@ MrPass mr_pass(const DevTables& T, int kind, long long n, long long na, long lon
     for (int q = 0; q < p.nf; ++q) p.fac[q] = T.fac[(size_t)q];
     p.root = T.mr_root;
     p.wq = T.mr_wq;
+    p.half = T.mr_half ? 1 : 0;
+    p.wt = T.mr_wt;
     p.perm = (const int*)T.mr_perm;
     p.out_mult = 1.0;
     const long long nl = na * nb;

@@ -144,6 +144,8 @@ struct MrPass {
     // pair's inverse transform; n_in follows kind, n_out follows ikind
     int mid, ikind;
     Scaling s;
+    int half;                   // even n, DCT/DST II-III or real FFT: complex FFT of length N = n/2
+    const void* wt;             // half: n/2 + 1 roots e^{-2 pi i k/n}
 };
 
 // the projection corrector (flow.py:125-139, 292-295):
