@@ -66,9 +66,10 @@ def test_golden_transforms_match_oracle(golden):
             assert np.abs(nv - y).max() <= 1e-11 * e["n"] * max(np.abs(x).max(), 1.0)
 
 
-@pytest.mark.parametrize("n", [8, 16, 64, 512, 4096])
+@pytest.mark.parametrize("n", [8, 16, 64, 512, 4096, 60, 250, 1000, 2046])
 def test_makhoul_recipes_match_scipy(n, rng):
-    # the half-length FFT recipes the GPU kernels implement
+    # the half-length FFT recipes the GPU kernels implement (FFT engine at 2^k, and the
+    # mixed-radix engine's half-length path at any even n)
     x = rng.standard_normal((3, n))
     np.testing.assert_allclose(orc.makhoul_dct2(x), orc.forward_1d("dct2", x), atol=1e-12 * n)
     np.testing.assert_allclose(orc.makhoul_dct3(x), orc.forward_1d("dct3", x), atol=1e-12 * n)
