@@ -289,6 +289,21 @@ __device__ __forceinline__ void mr_fill(const MrCtx<T>& c, int kind, bool lminor
                 const cx<T> xk = mkc<T>(q.x, k == 0 ? (T)0 : q.y), xm = mkc<T>(q.z, k == 0 ? (T)0 : q.w);
                 zall[l * slots + P(__ldg(&perm[k]))] = rmerge<T>(xk, xm, __ldg(&c.wt[k]));
             });
+        } else if (kind == FP_DCT1 || kind == FP_DST1) {
+            // the 2N-point even (DCT-I, n = N + 1) / odd (DST-I, n = N - 1) extension, packed
+            const int E = 2 * N;
+            mr_walk_batched<U>(lminor, n, c.logLT, [&](int l, int j) { return getR(l, j); }, [&](int l, int j, T x) {
+                if (chk && !finite_t(x)) bad = 1;
+                cx<T>* z = zall + l * slots;
+                if (kind == FP_DCT1) {
+                    put_half<T>(z, perm, j, x);
+                    if (j >= 1 && j <= N - 1) put_half<T>(z, perm, E - j, x);
+                } else {
+                    put_half<T>(z, perm, j + 1, x);
+                    put_half<T>(z, perm, E - 1 - j, -x);
+                    if (j == 0) { put_half<T>(z, perm, 0, (T)0); put_half<T>(z, perm, N, (T)0); }
+                }
+            });
         } else {
             // DCT-II / DST-II (Makhoul packing) and the real FFT (natural packing)
             mr_walk_batched<U>(lminor, n, c.logLT, [&](int l, int j) { return getR(l, j); }, [&](int l, int j, T x) {
@@ -355,6 +370,18 @@ template <typename T, bool HALF, typename PR, typename PC>
 __device__ __forceinline__ void mr_emit(const MrCtx<T>& c, int kind, bool lminor, int nout, PR&& putR, PC&& putC) {
     const int slots = c.slots, n = c.n;
     if constexpr (HALF) {
+        if (kind == FP_DCT1 || kind == FP_DST1) {
+            // real FFT of the extension: V_q = rsplit(Z_q, Z_{N-q}, e^{-2 pi i q/(2N)});
+            // DCT-I X_k = Re V_k (k <= N), DST-I X_k = -Im V_{k+1}
+            const int N = c.N;
+            mr_walk(lminor, nout, c.logLT, [&](int l, int k) {
+                const cx<T>* z = c.zall + l * slots;
+                const int q = kind == FP_DCT1 ? k : k + 1;
+                const cx<T> V = rsplit<T>(z[P(q == N ? 0 : q)], z[P(q == 0 ? 0 : N - q)], __ldg(&c.wt[q]));
+                putR(l, k, kind == FP_DCT1 ? V.x : -V.y);
+            });
+            return;
+        }
         const int M = n >> 1;
         mr_walk(lminor, nout, c.logLT, [&](int l, int k) {
             const cx<T>* z = c.zall + l * slots;
@@ -563,12 +590,12 @@ static MrKernelFn mr_pick_h(int kind, bool mid) {
             case FP_DCT2: return mr_pass_kernel<T, FP_DCT2, FP_DCT3, H>;
             case FP_DST2: return mr_pass_kernel<T, FP_DST2, FP_DST3, H>;
             case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, MR_IRFFT, H>;
+            case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, FP_DCT1, H>;
+            case FP_DST1: return mr_pass_kernel<T, FP_DST1, FP_DST1, H>;
             default: break;
         }
         if constexpr (!H) {
             switch (kind) {
-                case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, FP_DCT1, false>;
-                case FP_DST1: return mr_pass_kernel<T, FP_DST1, FP_DST1, false>;
                 case FP_DFT: return mr_pass_kernel<T, FP_DFT, FP_IDFT, false>;
                 default: break;
             }
@@ -582,14 +609,14 @@ static MrKernelFn mr_pick_h(int kind, bool mid) {
         case FP_DCT3: return mr_pass_kernel<T, FP_DCT3, -1, H>;
         case MR_RFFT: return mr_pass_kernel<T, MR_RFFT, -1, H>;
         case MR_IRFFT: return mr_pass_kernel<T, MR_IRFFT, -1, H>;
+        case FP_DST1: return mr_pass_kernel<T, FP_DST1, -1, H>;
+        case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, -1, H>;
         default: break;
     }
     if constexpr (!H) {
         switch (kind) {
             case FP_DFT: return mr_pass_kernel<T, FP_DFT, -1, false>;
             case FP_IDFT: return mr_pass_kernel<T, FP_IDFT, -1, false>;
-            case FP_DST1: return mr_pass_kernel<T, FP_DST1, -1, false>;
-            case FP_DCT1: return mr_pass_kernel<T, FP_DCT1, -1, false>;
             default: break;
         }
     }

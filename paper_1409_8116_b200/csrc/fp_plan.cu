@@ -240,20 +240,28 @@ fp_status upload_ints(AllocT& allocs, const std::vector<int>& v, void** out) {
 
 // complex FFT length of a mixed-radix line of transform `kind` (FP_* id, or
 // MR_RFFT / MR_IRFFT); 0 if the length has no mixed-radix plan in this build
-bool mr_half_kind(int kind, long long n) {
+// complex FFT length of the half-length recipe (0: none): n/2 for even-n II/III
+// kinds and the real FFT; n - 1 / n + 1 (half the type-I extension) for DCT-I / DST-I
+long long mr_half_length(int kind, long long n) {
     static const bool on = [] { const char* v = std::getenv("FP_MR_HALF"); return !(v && *v == '0'); }();
-    const bool k2 = kind == FP_DCT2 || kind == FP_DST2 || kind == FP_DCT3 || kind == FP_DST3 ||
-                    kind == MR_RFFT || kind == MR_IRFFT;
-    return on && k2 && n % 2 == 0 && n / 2 >= 8 && !mr_factors(n / 2, kMrMaxPrime).empty();
+    if (!on) return 0;
+    long long h = 0;
+    if (kind == FP_DCT2 || kind == FP_DST2 || kind == FP_DCT3 || kind == FP_DST3 || kind == MR_RFFT || kind == MR_IRFFT)
+        h = (n % 2 == 0) ? n / 2 : 0;
+    else if (kind == FP_DCT1) h = n - 1;
+    else if (kind == FP_DST1) h = n + 1;
+    if (h < 8 || mr_factors(h, kMrMaxPrime).empty()) return 0;
+    return h;
 }
+bool mr_half_kind(int kind, long long n) { return mr_half_length(kind, n) > 0; }
 
 long long mr_length(int kind, long long n, bool f32) {
     static const bool on = [] { const char* v = std::getenv("FP_MR"); return !(v && *v == '0'); }();
     if (!on || n < 16) return 0;   // short lines: the dense engine
     long long N = n;
-    if (mr_half_kind(kind, n)) N = n / 2;
     if (kind == FP_DCT1) N = 2 * (n - 1);
     if (kind == FP_DST1) N = 2 * (n + 1);
+    if (mr_half_kind(kind, n)) N = mr_half_length(kind, n);
     if (mr_factors(N, kMrMaxPrime).empty()) return 0;
     const size_t line = (size_t)(N + (N - 1) / 16 + 1) * (f32 ? 8 : 16);
     if (line > 200 * 1024) return 0;
@@ -288,7 +296,8 @@ fp_status mr_setup(AllocT& allocs, DevTables& T, int kind, long long n, bool f32
     root_table(4 * n, n + 1, r);   // e^{-i pi k/(2n)}
     if ((st = upload(allocs, r, f32, &T.mr_wq)) != FP_OK) return st;
     if (T.mr_half) {
-        root_table(n, n / 2 + 1, r);   // e^{-2 pi i k/n}
+        // e^{-2 pi i k/(2N)}, k <= N: the real-FFT untangle of the packed line (2N reals)
+        root_table(2 * N, N + 1, r);
         if ((st = upload(allocs, r, f32, &T.mr_wt)) != FP_OK) return st;
     }
     if ((st = upload_ints(allocs, mr_perm((int)N, T.fac), &T.mr_perm)) != FP_OK) return st;

@@ -68,10 +68,16 @@ def test_transform_beyond_dense_limit(kind, n, precision, torch_cuda, rng):
     _check_transform(kind, n, 0, [n, 3], torch_cuda, rng, precision=precision)
 
 
-def test_fp64_type1_beyond_shared_memory_is_unsupported(torch_cuda):
-    # 2(n - 1) = 18000 complex fp64 points do not fit one CTA: NotImplementedError, no fallback
+@pytest.mark.parametrize("kind,n", [(fp.TransformKind.DCT1, 9001), (fp.TransformKind.DST1, 9999)])
+def test_fp64_type1_beyond_dense_limit(kind, n, torch_cuda, rng):
+    # type I on the half-length recipe: the 2(n -+ 1)-point extension packed into n -+ 1 complex points
+    _check_transform(kind, n, 0, [n, 3], torch_cuda, rng)
+
+
+def test_large_prime_length_is_unsupported(torch_cuda):
+    # 8209 is prime: no mixed-radix plan, beyond the dense engine -> NotImplementedError, no fallback
     with pytest.raises(NotImplementedError):
-        fp.TransformPlan(fp.TransformKind.DCT1, 9001, axis=0).execute(torch_cuda.zeros((9001, 2), dtype=torch_cuda.float64, device="cuda"))
+        fp.TransformPlan(fp.TransformKind.DCT2, 8209, axis=0).execute(torch_cuda.zeros((8209, 2), dtype=torch_cuda.float64, device="cuda"))
 
 
 def _solve_case(axes, approx, precision, torch_cuda, rng, device=False):
