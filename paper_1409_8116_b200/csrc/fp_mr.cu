@@ -383,6 +383,19 @@ __device__ __forceinline__ void mr_emit(const MrCtx<T>& c, int kind, bool lminor
             return;
         }
         const int M = n >> 1;
+        if (kind == FP_DCT2 || kind == FP_DST2) {
+            // one untangle per pair: U_q = w_q V_q gives X_q = 2 Re U_q and X_{n-q} = -2 Im U_q
+            // (DST-II: at the mirrored physical indices)
+            const bool dst = kind == FP_DST2;
+            mr_walk(lminor, M + 1, c.logLT, [&](int l, int q) {
+                const cx<T>* z = c.zall + l * slots;
+                const cx<T> V = rsplit<T>(z[P(q == M ? 0 : q)], z[P(q == 0 ? 0 : M - q)], __ldg(&c.wt[q]));
+                const cx<T> U = cmul<T>(__ldg(&c.wq[q]), V);
+                putR(l, dst ? n - 1 - q : q, (T)2 * U.x);
+                if (q >= 1 && q < M) putR(l, dst ? q - 1 : n - q, (T)-2 * U.y);
+            });
+            return;
+        }
         mr_walk(lminor, nout, c.logLT, [&](int l, int k) {
             const cx<T>* z = c.zall + l * slots;
             if (kind == MR_RFFT || kind == FP_DCT2 || kind == FP_DST2) {
