@@ -263,10 +263,11 @@ __device__ __forceinline__ void mr_fill(const MrCtx<T>& c, int kind, bool lminor
     if constexpr (HALF) {
         const int M = n >> 1;
         if (kind == FP_DCT3 || kind == FP_DST3) {
-            // Z_k = rmerge(V_k, V_{M-k}, t_k), V_k = conj(w_k)(X'_k - i X'_{n-k}) (V_0 = X'_0), k < M
+            // Z_k = rmerge(V_k, V_{M-k}, t_k), V_k = conj(w_k)(X'_k - i X'_{n-k}) (V_0 = X'_0);
+            // one thread builds the pair (Z_k, Z_{M-k}), k <= M/2
             const bool dst = kind == FP_DST3;
             auto xp = [&](int l, int k) { return getR(l, dst ? n - 1 - k : k); };   // X'_k, k < n
-            mr_walk_batched<U>(lminor, M, c.logLT, [&](int l, int k) {
+            mr_walk_batched<U>(lminor, M / 2 + 1, c.logLT, [&](int l, int k) {
                 // X'_k, X'_{n-k} (0 at k = 0), X'_{M-k}, X'_{M+k}
                 return make_double4_t<T>(xp(l, k), k > 0 ? xp(l, n - k) : (T)0, xp(l, M - k), xp(l, M + k));
             }, [&](int l, int k, typename Quad<T>::type q) {
@@ -277,17 +278,21 @@ __device__ __forceinline__ void mr_fill(const MrCtx<T>& c, int kind, bool lminor
                     return mkc<T>(w.x * a - w.y * b, -w.y * a - w.x * b);
                 };
                 const cx<T> vk = V(k, q.x, q.y), vm = V(M - k, q.z, q.w);
-                zall[l * slots + P(__ldg(&perm[k]))] = rmerge<T>(vk, vm, __ldg(&c.wt[k]));
+                cx<T>* z = zall + l * slots;
+                z[P(__ldg(&perm[k]))] = rmerge<T>(vk, vm, __ldg(&c.wt[k]));
+                if (k > 0 && 2 * k != M) z[P(__ldg(&perm[M - k]))] = rmerge<T>(vm, vk, __ldg(&c.wt[M - k]));
             });
         } else if (kind == MR_IRFFT) {
-            mr_walk_batched<U>(lminor, M, c.logLT, [&](int l, int k) {
+            mr_walk_batched<U>(lminor, M / 2 + 1, c.logLT, [&](int l, int k) {
                 const cx<T> a = getC(l, k), b = getC(l, M - k);
                 return make_double4_t<T>(a.x, a.y, b.x, b.y);
             }, [&](int l, int k, typename Quad<T>::type q) {
                 if (chk && !(finite_t(q.x) && finite_t(q.y) && finite_t(q.z) && finite_t(q.w))) bad = 1;
                 // the DC / Nyquist imaginary parts do not enter a real inverse (dense kind 101)
                 const cx<T> xk = mkc<T>(q.x, k == 0 ? (T)0 : q.y), xm = mkc<T>(q.z, k == 0 ? (T)0 : q.w);
-                zall[l * slots + P(__ldg(&perm[k]))] = rmerge<T>(xk, xm, __ldg(&c.wt[k]));
+                cx<T>* z = zall + l * slots;
+                z[P(__ldg(&perm[k]))] = rmerge<T>(xk, xm, __ldg(&c.wt[k]));
+                if (k > 0 && 2 * k != M) z[P(__ldg(&perm[M - k]))] = rmerge<T>(xm, xk, __ldg(&c.wt[M - k]));
             });
         } else if (kind == FP_DCT1 || kind == FP_DST1) {
             // the 2N-point even (DCT-I, n = N + 1) / odd (DST-I, n = N - 1) extension, packed
