@@ -46,15 +46,28 @@ template <typename T>
 __device__ __forceinline__ cx<T> conj_if(cx<T> w, bool c) { return c ? mkc<T>(w.x, -w.y) : w; }
 
 // odd prime radix R (compile time) or generic (R = 0: runtime r, local arrays)
+// cos / sin (2 pi m / R) for the compile-time radices, correctly rounded
+__device__ __forceinline__ constexpr double odd_cos(int R, int m) {
+    return R == 3 ? -0.5
+         : R == 5 ? (m == 1 ? 0.30901699437494742410 : -0.80901699437494742410)
+                  : (m == 1 ? 0.62348980185873353053 : m == 2 ? -0.22252093395631440429 : -0.90096886790241912624);
+}
+__device__ __forceinline__ constexpr double odd_sin(int R, int m) {
+    return R == 3 ? 0.86602540378443864676
+         : R == 5 ? (m == 1 ? 0.95105651629515357212 : 0.58778525229247312917)
+                  : (m == 1 ? 0.78183148246802980871 : m == 2 ? 0.97492791218182360702 : 0.43388373911755812048);
+}
+
 template <typename T, int R>
 __device__ __forceinline__ void dft_odd(cx<T>* a, const cx<T>* __restrict__ root, int N, bool inv) {
     constexpr int H = (R - 1) / 2;
     T C[H + 1], S[H + 1];
+    (void)root;
+    (void)N;
 #pragma unroll
     for (int m = 1; m <= H; ++m) {
-        const cx<T> w = __ldg(&root[m * (N / R)]);   // e^{-2 pi i m/R}
-        C[m] = w.x;
-        S[m] = inv ? w.y : -w.y;                     // forward: sin; inverse: -sin
+        C[m] = (T)odd_cos(R, m);
+        S[m] = inv ? (T)-odd_sin(R, m) : (T)odd_sin(R, m);   // forward: sin; inverse: -sin
     }
     cx<T> p[H + 1], q[H + 1];
     cx<T> x0 = a[0];
