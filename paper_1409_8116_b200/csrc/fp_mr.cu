@@ -134,8 +134,14 @@ __device__ __forceinline__ void mr_bfly(cx<T>* z, int base, int L, int k1, int s
 #pragma unroll
     for (int r = 0; r < R; ++r) a[r] = z[P(base + r * L)];
     if (k1 != 0) {
+        // one root load, the other powers by multiplication (the engine is LSU-bound,
+        // its fp64 pipe mostly idle): w^r = (w^(r/2))^2 or w^(r-1) w
+        cx<T> tw[R];
+        tw[1] = conj_if<T>(__ldg(&root[k1 * step]), inv);
 #pragma unroll
-        for (int r = 1; r < R; ++r) a[r] = cmul<T>(a[r], conj_if<T>(__ldg(&root[r * k1 * step]), inv));
+        for (int r = 2; r < R; ++r) tw[r] = (r & 1) ? cmul<T>(tw[r - 1], tw[1]) : cmul<T>(tw[r / 2], tw[r / 2]);
+#pragma unroll
+        for (int r = 1; r < R; ++r) a[r] = cmul<T>(a[r], tw[r]);
     }
     if constexpr (R == 2 || R == 4 || R == 8 || R == 16) {
         if (inv) dft_reg<R, true, T>(a);
