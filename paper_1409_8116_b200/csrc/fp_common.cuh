@@ -130,7 +130,9 @@ __host__ __device__ constexpr int stage_tw_total(int logM) { return stage_tw_off
 #endif
 template <typename T> inline constexpr bool kTwoLevelTwiddles = sizeof(T) == 4 ? FP_TW2_F32 : FP_TW2_F64;
 
-template <int R, int LOGNS, bool INV, typename T, int LOGM, bool FROM_REG = false, bool TO_REG = false>
+// TWP: radix-16 twiddles from two table loads (w, w^4) and products instead of six
+// loads -- for the LSU-bound passes; the fp64-bound real-line MID keeps the loads
+template <int R, int LOGNS, bool INV, typename T, int LOGM, bool FROM_REG = false, bool TO_REG = false, bool TWP = false>
 __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* __restrict__ W,
                                                cx<T>* vio = nullptr) {
     // FROM_REG: butterfly inputs come from vio[s] = z[jt + TL s] (the layout the
@@ -157,8 +159,14 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* 
                 // two-level twiddles: load w^r for r in {1,2,3,4,8,12} and form the
                 // other nine as w^(r&3) * w^(r&12) (6 loads instead of 15)
                 cx<T> w[16];
-                w[1] = __ldg(&tw[NS]); w[2] = __ldg(&tw[2 * NS]); w[3] = __ldg(&tw[3 * NS]);
-                w[4] = __ldg(&tw[4 * NS]); w[8] = __ldg(&tw[8 * NS]); w[12] = __ldg(&tw[12 * NS]);
+                if constexpr (TWP) {
+                    w[1] = __ldg(&tw[NS]); w[4] = __ldg(&tw[4 * NS]);
+                    w[2] = cmul<T>(w[1], w[1]); w[3] = cmul<T>(w[2], w[1]);
+                    w[8] = cmul<T>(w[4], w[4]); w[12] = cmul<T>(w[8], w[4]);
+                } else {
+                    w[1] = __ldg(&tw[NS]); w[2] = __ldg(&tw[2 * NS]); w[3] = __ldg(&tw[3 * NS]);
+                    w[4] = __ldg(&tw[4 * NS]); w[8] = __ldg(&tw[8 * NS]); w[12] = __ldg(&tw[12 * NS]);
+                }
 #pragma unroll
                 for (int h = 4; h < 16; h += 4)
 #pragma unroll
@@ -192,52 +200,52 @@ __device__ __forceinline__ void stockham_stage(cx<T>* line, int jt, const void* 
     __syncthreads();
 }
 
-template <int LOGNS, bool INV, typename T, int LOGM>
+template <int LOGNS, bool INV, typename T, int LOGM, bool TWP = false>
 __device__ __forceinline__ void radix16_stages(cx<T>* line, int jt, const void* __restrict__ W) {
     if constexpr (LOGNS < LOGM) {
-        stockham_stage<16, LOGNS, INV, T, LOGM>(line, jt, W);
-        radix16_stages<LOGNS + 4, INV, T, LOGM>(line, jt, W);
+        stockham_stage<16, LOGNS, INV, T, LOGM, false, false, TWP>(line, jt, W);
+        radix16_stages<LOGNS + 4, INV, T, LOGM, TWP>(line, jt, W);
     }
 }
 
-template <bool INV, typename T, int LOGM>
+template <bool INV, typename T, int LOGM, bool TWP = false>
 __device__ __forceinline__ void fft_tile(cx<T>* line, int jt, const void* __restrict__ W) {
     constexpr int REM = LOGM & 3;
     if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
-    radix16_stages<REM, INV, T, LOGM>(line, jt, W);
+    radix16_stages<REM, INV, T, LOGM, TWP>(line, jt, W);
 }
 
-template <int LOGNS, int LIMIT, bool INV, typename T, int LOGM>
+template <int LOGNS, int LIMIT, bool INV, typename T, int LOGM, bool TWP = false>
 __device__ __forceinline__ void radix16_stages_upto(cx<T>* line, int jt, const void* __restrict__ W) {
     if constexpr (LOGNS < LIMIT) {
-        stockham_stage<16, LOGNS, INV, T, LOGM>(line, jt, W);
-        radix16_stages_upto<LOGNS + 4, LIMIT, INV, T, LOGM>(line, jt, W);
+        stockham_stage<16, LOGNS, INV, T, LOGM, false, false, TWP>(line, jt, W);
+        radix16_stages_upto<LOGNS + 4, LIMIT, INV, T, LOGM, TWP>(line, jt, W);
     }
 }
 
 // all stages; the last (radix-16, Ns = TL) keeps its outputs in registers:
 // v[r] = Z[jt + TL r]
-template <bool INV, typename T, int LOGM>
+template <bool INV, typename T, int LOGM, bool TWP = false>
 __device__ __forceinline__ void fft_tile_to_reg(cx<T>* line, int jt, const void* __restrict__ W, cx<T>* v) {
     constexpr int REM = LOGM & 3;
     if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM>(line, jt, W);
     if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM>(line, jt, W);
     constexpr int FIRST16 = REM;
-    if constexpr (LOGM - 4 > FIRST16) radix16_stages_upto<FIRST16, LOGM - 4, INV, T, LOGM>(line, jt, W);
-    stockham_stage<16, LOGM - 4, INV, T, LOGM, false, true>(line, jt, W, v);
+    if constexpr (LOGM - 4 > FIRST16) radix16_stages_upto<FIRST16, LOGM - 4, INV, T, LOGM, TWP>(line, jt, W);
+    stockham_stage<16, LOGM - 4, INV, T, LOGM, false, true, TWP>(line, jt, W, v);
 }
 
 // all stages; the first takes its inputs from registers v[s] = z[jt + TL s]
-template <bool INV, typename T, int LOGM>
+template <bool INV, typename T, int LOGM, bool TWP = false>
 __device__ __forceinline__ void fft_tile_from_reg(cx<T>* line, int jt, const void* __restrict__ W, cx<T>* v) {
     constexpr int REM = LOGM & 3;
-    if constexpr (REM == 1) { stockham_stage<2, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<1, INV, T, LOGM>(line, jt, W); }
-    if constexpr (REM == 2) { stockham_stage<4, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<2, INV, T, LOGM>(line, jt, W); }
-    if constexpr (REM == 3) { stockham_stage<8, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<3, INV, T, LOGM>(line, jt, W); }
-    if constexpr (REM == 0) { stockham_stage<16, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<4, INV, T, LOGM>(line, jt, W); }
+    if constexpr (REM == 1) { stockham_stage<2, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<1, INV, T, LOGM, TWP>(line, jt, W); }
+    if constexpr (REM == 2) { stockham_stage<4, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<2, INV, T, LOGM, TWP>(line, jt, W); }
+    if constexpr (REM == 3) { stockham_stage<8, 0, INV, T, LOGM, true>(line, jt, W, v); radix16_stages<3, INV, T, LOGM, TWP>(line, jt, W); }
+    if constexpr (REM == 0) { stockham_stage<16, 0, INV, T, LOGM, true, false, TWP>(line, jt, W, v); radix16_stages<4, INV, T, LOGM, TWP>(line, jt, W); }
 }
 
 // twiddles of the mirrored index M-q from those of q (n = 2M):

@@ -46,6 +46,13 @@ __device__ __forceinline__ int line_stride(const FftPass& p) {
 __host__ __device__ constexpr int opb(int op) { return op & 15; }
 __host__ __device__ constexpr int opkind(int op) { return (op >> 4) - 1; }
 __host__ __device__ constexpr int mid_op(int kind) { return OP_MID | ((kind + 1) << 4); }
+// radix-16 twiddle source per pass: products of two loads for the LSU-bound fp64
+// passes (c4 11.24 -> 11.11 ms), six loads for the fp64-bound MID of real lines
+// (kind-specialised DCT / DST / rFFT: 0.713 -> 0.820 ms with products) and for fp32
+// (the products' extra rounding costs the 2048^3 planted-mode check its 1e-5 margin)
+template <typename T, int OP>
+inline constexpr bool kTwPow = sizeof(T) == 8 && !(opb(OP) == OP_MID && opkind(OP) >= 0 && opkind(OP) != FK_CFFT);
+
 template <int OP>
 __device__ __forceinline__ int fkind_of(const FftPass& p) {
     if constexpr (opkind(OP) >= 0) return opkind(OP);
@@ -650,7 +657,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
             const double cst = Sc.bscale * Sc.inv_np;
             cx<T> v[16];
-            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            fft_tile_to_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
             if (jt == 0) {
                 if (cap) *Sc.dc_out = (double)v[0].x;
                 v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
@@ -659,14 +666,14 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             }
 #pragma unroll
             for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
-            fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+            fft_tile_from_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
             compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
             return;
         }
     }
 
     if constexpr (fwd_in) {
-        fft_tile<false, T, LOGM>(line_f, jt, W);
+        fft_tile<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W);
 
         if constexpr (opb(OP) == OP_FWD) {
             const int kind = fkind_of<OP>(p);
@@ -1000,7 +1007,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
 
     if constexpr (opb(OP) != OP_FWD) {
         // =============== INVERSE FFT + store (INV and MID)
-        fft_tile<true, T, LOGM>(line_f, jt, W);
+        fft_tile<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W);
         compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
     }
 }
@@ -1061,7 +1068,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
 
     if constexpr (opb(OP) == OP_FWD) {
         // CONTIG only: I/O mapping == line-major mapping
-        fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+        fft_tile_to_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         const LineInfo L = linfo[lf];
         const int kind = fkind_of<OP>(p);
         const T om = (T)p.out_mult;
@@ -1123,7 +1130,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         return;
     } else {
         if constexpr (opb(OP) == OP_MID) {
-            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            fft_tile_to_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
             const int kind = fkind_of<OP>(p);
             const Scaling& Sc = p.s;
             const LineInfo L = linfo[lf];
@@ -1252,7 +1259,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         }
         // inverse FFT from registers (its first write is preceded by a barrier,
         // so the pre-processing reads above are complete)
-        fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+        fft_tile_from_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
     }
 }
@@ -1329,7 +1336,7 @@ __global__ void __launch_bounds__(512) fft_pass_wide(const FftPass p) {
             const LineInfo L = linfo[lf];
             const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
             cx<T> v[16];
-            fft_tile_to_reg<false, T, LOGM>(line_f, jt, W, v);
+            fft_tile_to_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
             if (jt == 0) {
                 if (cap) *Sc.dc_out = (double)v[0].x;
                 v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
@@ -1338,9 +1345,9 @@ __global__ void __launch_bounds__(512) fft_pass_wide(const FftPass p) {
             }
 #pragma unroll
             for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
-            fft_tile_from_reg<true, T, LOGM>(line_f, jt, W, v);
+            fft_tile_from_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         } else {
-            fft_tile<opb(OP) == OP_INV, T, LOGM>(line_f, jt, W);
+            fft_tile<opb(OP) == OP_INV, T, LOGM, kTwPow<T, OP>>(line_f, jt, W);
         }
     }
     if constexpr (opb(OP) == OP_FWD) {
