@@ -50,6 +50,26 @@ __host__ __device__ constexpr int mid_op(int kind) { return OP_MID | ((kind + 1)
 // passes (c4 11.24 -> 11.11 ms), six loads for the fp64-bound MID of real lines
 // (kind-specialised DCT / DST / rFFT: 0.713 -> 0.820 ms with products) and for fp32
 // (the products' extra rounding costs the 2048^3 planted-mode check its 1e-5 margin)
+// quad post / pre-processing twiddles t_q, w_q (q = jt + TL r) as running products
+// of t_jt, w_jt by t_TL, w_TL in the fp64 forward / inverse passes (2 + 2 loads
+// instead of 16)
+template <typename T, int OP>
+inline constexpr bool kTwPowQ = sizeof(T) == 8 && opb(OP) != OP_MID;
+template <typename T, bool PROD>
+struct QuadTw {
+    cx<T> t, w, dt, dw;
+    const cx<T>* Wt;
+    const cx<T>* Ww;
+    __device__ __forceinline__ QuadTw(const cx<T>* wt, const cx<T>* ww, int jt, int TL) : Wt(wt), Ww(ww) {
+        if constexpr (PROD) { t = Wt[jt]; w = Ww ? Ww[jt] : mkc<T>(1, 0); dt = Wt[TL]; dw = Ww ? Ww[TL] : mkc<T>(1, 0); }
+    }
+    // twiddles of q (PROD: the running value for the current r), then step to r + 1
+    __device__ __forceinline__ void get(int q, cx<T>& tq, cx<T>& wq) {
+        if constexpr (PROD) { tq = t; wq = w; t = cmul<T>(t, dt); w = cmul<T>(w, dw); }
+        else { tq = Wt[q]; wq = Ww ? Ww[q] : mkc<T>(1, 0); }
+    }
+};
+
 template <typename T, int OP>
 inline constexpr bool kTwPow = sizeof(T) == 8 && !(opb(OP) == OP_MID && opkind(OP) >= 0 && opkind(OP) != FK_CFFT);
 
@@ -1086,16 +1106,18 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         if (kind == FK_RFFT) {
             cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + L.out_off;
             const T omh = om * (T)0.5;
+            QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, jt, TL);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int q = jt + r * TL;
+                cx<T> tq, wq_unused;
+                qt.get(q, tq, wq_unused);
                 if (r == 0 && jt == 0) {
                     const cx<T> z0 = v[0], zh = v[8];
                     pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
                     pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
                     pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
                 } else {
-                    const cx<T> tq = Wt[q];
                     pb[(long long)q * os] = cscale<T>(rsplit2<T>(v[r], pz[r], tq), omh);
                     pb[(long long)(M - q) * os] = cscale<T>(rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)), omh);
                 }
@@ -1105,9 +1127,12 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
             T* const pb = reinterpret_cast<T*>(g.out) + L.out_off;
             const long long s1 = dst ? -os : os;
             T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;
+            QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
                 const int q = jt + r * TL;
+                cx<T> tq, wq;
+                qt.get(q, tq, wq);
                 if (r == 0 && jt == 0) {
                     const cx<T> z0 = v[0], zh = v[8];
                     const cx<T> wM = Ww[M];
@@ -1117,7 +1142,6 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
                     p0[(long long)HALF * s1] = U.x * om;
                     p0[(long long)(n - HALF) * s1] = -U.y * om;
                 } else {
-                    const cx<T> tq = Wt[q], wq = Ww[q];
                     const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
                     const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)));
                     p0[(long long)q * s1] = U1.x * om;
@@ -1218,25 +1242,30 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
             const int ik = ikind_of<OP>(p);
             cx<T> half0 = mkc<T>(0, 0);
             if (ik == IK_IRFFT) {
+                QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, jt, TL);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int q = jt + r * TL;
+                    cx<T> tq, wq_unused;
+                    qt.get(q, tq, wq_unused);
                     if (r == 0 && jt == 0) {
                         const cx<T> x0 = line_f[P(0)], xM = line_f[P(M)], xh = line_f[P(HALF)];
                         v[0] = rmerge<T>(x0, xM, mkc<T>(1, 0));
                         half0 = rmerge<T>(xh, xh, Wt[HALF]);
                     } else {
                         const cx<T> xk = line_f[P(q)], xm = line_f[P(M - q)];
-                        const cx<T> tq = Wt[q];
                         v[r] = rmerge<T>(xk, xm, tq);
                         pz[r] = rmerge<T>(xm, xk, t_mirror<T>(tq));
                     }
                 }
             } else {
                 const T* zr = reinterpret_cast<const T*>(line_f);
+                QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
 #pragma unroll
                 for (int r = 0; r < 8; ++r) {
                     const int q = jt + r * TL;
+                    cx<T> tq0, wq0;
+                    qt.get(q, tq0, wq0);
                     if (r == 0 && jt == 0) {
                         const T X0 = zr[PR(0)], XM = zr[PR(M)];
                         const cx<T> wM = Ww[M];
@@ -1246,8 +1275,8 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
                         const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
                         half0 = rmerge<T>(Vh, Vh, th);
                     } else {
-                        const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                        const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                        const cx<T> wq = wq0, wm = w_mirror<T>(wq);
+                        const cx<T> tq = tq0, tm = t_mirror<T>(tq);
                         const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
                         const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
                         v[r] = rmerge<T>(Vk, Vm, tq);
