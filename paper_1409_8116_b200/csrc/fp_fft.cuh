@@ -718,9 +718,12 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                         cx<T>* pq = pb + (long long)(8 * b) * os;
                         cx<T>* pm = pb + (long long)(M - 8 * b) * os;
                         const T omh = om * (T)0.5;
+                        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, 8 * b, 1);   // q = 8b + it: step t_1
 #pragma unroll
                         for (int it = 0; it < 8; ++it, pq += os, pm -= os) {
                             const int q = 8 * b + it;
+                            cx<T> tq, wq_unused;
+                            qt.get(q, tq, wq_unused);
                             if (it == 0 && b == 0) {
                                 const cx<T> z0 = line_io[P(0)];
                                 pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
@@ -729,7 +732,6 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                                 pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
                             } else {
                                 const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
-                                const cx<T> tq = Wt[q];
                                 *pq = cscale<T>(rsplit2<T>(zk, zm, tq), omh);
                                 *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
                             }
@@ -755,9 +757,12 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                         T* pn = p0 + (long long)(n - 8 * b) * s1;
                         T* pm = p0 + (long long)(M - 8 * b) * s1;
                         T* pp = p0 + (long long)(M + 8 * b) * s1;
+                        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, 8 * b, 1);   // q = 8b + it: steps t_1, w_1
 #pragma unroll
                         for (int it = 0; it < 8; ++it, pa += s1, pn -= s1, pm -= s1, pp += s1) {
                             const int q = 8 * b + it;
+                            cx<T> tq, wq;
+                            qt.get(q, tq, wq);
                             if (it == 0 && b == 0) {
                                 const cx<T> z0 = line_io[P(0)];
                                 const cx<T> wM = Ww[M];
@@ -769,7 +774,6 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                                 p0[(long long)(n - HALF) * s1] = -U.y * om;
                             } else {
                                 const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
-                                const cx<T> tq = Wt[q], wq = Ww[q];
                                 const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
                                 const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
                                 *pa = U1.x * om;
