@@ -842,9 +842,11 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                     T* pm = p0 + (long long)(M - bio) * s1;       // k = M - q
                     T* pp = p0 + (long long)(M + bio) * s1;       // k = M + q
                     const long long step = (long long)TL * s1;
+                    QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, bio, TL);   // q = bio + TL it, ascending
                     auto quad = [&](int q) {
                         const cx<T> zk = line_io[P(q)], zm = line_io[P(M - q)];
-                        const cx<T> tq = Wt[q], wq = Ww[q];
+                        cx<T> tq, wq;
+                        qt.get(q, tq, wq);
                         const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));        // X_q = Re, X_{n-q} = -Im
                         const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
                         *pa = U1.x * om;
@@ -861,6 +863,8 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                         const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
                         p0[(long long)HALF * s1] = U.x * om;
                         p0[(long long)(n - HALF) * s1] = -U.y * om;
+                        cx<T> t0, w0;
+                        qt.get(0, t0, w0);   // keep the running twiddles in step
                     } else {
                         quad(bio);
                     }
@@ -977,9 +981,12 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             // two-phase: the real-valued view overlaps the complex slots
             const T* zr = reinterpret_cast<const T*>(line_f);
             cx<T> hold[16];
+            QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);   // q = jt + TL it, ascending
             auto quad = [&](int q, int it) {
-                const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
+                cx<T> tq, wq;
+                qt.get(q, tq, wq);
+                const cx<T> wm = w_mirror<T>(wq);
+                const cx<T> tm = t_mirror<T>(tq);
                 const cx<T> Vk = cmulc<T>(mkc<T>(zr[PR(q)], -zr[PR(n - q)]), wq);
                 const cx<T> Vm = cmulc<T>(mkc<T>(zr[PR(M - q)], -zr[PR(M + q)]), wm);
                 hold[2 * it] = rmerge<T>(Vk, Vm, tq);
@@ -993,6 +1000,8 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                 const cx<T> wh = Ww[HALF], th = Wt[HALF];
                 const cx<T> Vh = cmulc<T>(mkc<T>(zr[PR(HALF)], -zr[PR(n - HALF)]), wh);
                 hold[1] = rmerge<T>(Vh, Vh, th);
+                cx<T> t0, w0;
+                qt.get(0, t0, w0);   // keep the running twiddles in step
             } else {
                 quad(jt, 0);
             }
