@@ -8,9 +8,11 @@ so no explicit flush is needed between steps).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
 
---impl reference times the reference algorithm on the host cores (the oracle
-port in oracle/, which calls scipy.fft exactly like the reference) on the same
-workload.  Under torchrun (N > 1) the ranks solve ONE global grid together:
+--impl reference times the reference's own CPU solve on the host cores: the
+unmodified reference package installed in baseline/_ref (its SolverPlan built
+once, then SolverPlan.solve per step, threads = all cores; one extra
+single-thread solve is reported as t1), falling back to the oracle port when
+baseline/_ref is absent.  Under torchrun (N > 1) the ranks solve ONE global grid together:
 slab decomposition along axis 0, two NCCL all-to-alls per solve (strong
 scaling), reported against both the HBM and the NVLink rooflines.
 """
@@ -110,66 +112,227 @@ def dist_env():
     return ws, rank, local
 
 
+# BASELINE.json configs: per-axis (n, length, bc, grid kind), approximation, precision
+TWO_PI = 2.0 * np.pi
+BENCH_CONFIGS = {
+    "c1": ([(64, TWO_PI, "periodic", "regular")] * 3, "spectral", "double"),
+    "c2": ([(4096, 1.0, "dirichlet", "staggered")] * 2, "fd2", "double"),
+    "c3": ([(512, 1.0, "neumann", "staggered")] * 3, "fd2", "double"),
+    "c4": ([(1024, TWO_PI, "periodic", "regular"), (1024, TWO_PI, "periodic", "regular"),
+            (512, 2.0, "neumann", "staggered")], "fd2", "double"),
+    "c5": ([(2048, TWO_PI, "periodic", "regular")] * 3, "spectral", "single"),
+}
+# c5's reference solve needs ~270 GB of host RAM (dense _inv_lam + complex work arrays):
+# its CPU baseline runs on the labelled 1024^3 fp32 proxy
+CPU_PROXY = {"c5": 2}
+
+
+def config_axes(name, scale=1):
+    axes, approx, precision = BENCH_CONFIGS[name]
+    return [(n // scale, length, bc, kind) for n, length, bc, kind in axes], approx, precision
+
+
+def build_config(mod, name, scale=1):
+    """SolverConfig of the named workload from a package with the reference's API
+    (ours or the reference itself)."""
+    axes, approx, precision = config_axes(name, scale)
+    grids = tuple(mod.GridSpec(n, length, mod.BoundaryCondition(bc), mod.GridKind(kind)) for n, length, bc, kind in axes)
+    return mod.SolverConfig(grids, mod.Approximation(approx), precision)
+
+
 def make_config(name):
     import paper_1409_8116_b200 as fp
-    from oracle import fastpoisson_oracle as orc  # config table only (shapes / BCs)
 
-    case = orc.config_case(name)
-    grids = tuple(fp.GridSpec(a.n, a.length, fp.BoundaryCondition(a.bc), fp.GridKind(a.kind)) for a in case.axes)
-    return fp.SolverConfig(grids, fp.Approximation(case.approx), case.precision), case
+    return build_config(fp, name), None
+
+
+def host_rhs(name, config, seed=0):
+    """Seeded host RHS with the distribution BASELINE.json names."""
+    rng = np.random.default_rng(seed)
+    shape = config.shape
+    if name == "c2":
+        x = config.grids[0].points()
+        y = config.grids[1].points()
+        return rng.standard_normal(shape) + np.sin(np.pi * x)[:, None] * np.sin(np.pi * y)[None, :]
+    if name == "c4":
+        dx, dy, dz = (g.dx for g in config.grids)
+        u = rng.standard_normal(shape)
+        v = rng.standard_normal(shape)
+        w = rng.standard_normal(shape[:2] + (shape[2] + 1,))
+        w[..., 0] = 0.0
+        w[..., -1] = 0.0
+        return (np.roll(u, -1, 0) - u) / dx + (np.roll(v, -1, 1) - v) / dy + (w[..., 1:] - w[..., :-1]) / dz
+    if config.precision == "single":
+        r = rng.standard_normal(shape, dtype=np.float32)
+        r -= np.float32(r.astype(np.float64).mean())
+        return r
+    r = rng.standard_normal(shape)
+    return r - r.mean()
+
+
+def load_reference():
+    """The unmodified reference package installed in baseline/_ref (pip --target,
+    DESIGN.md section 5); None when it is not there."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if not (ref_dir / "fastpoisson" / "__init__.py").exists():
+        return None
+    sys.path.insert(0, str(ref_dir))
+    try:
+        import fastpoisson
+    except Exception:  # pragma: no cover
+        return None
+    finally:
+        sys.path.remove(str(ref_dir))
+    return fastpoisson
+
+
+class _PortPlan:
+    """Fallback when baseline/_ref is absent: the oracle port with its plan-time
+    arrays built once (the reference's SolverPlan.__init__, solver.py:136-181)."""
+
+    def __init__(self, name, scale, threads):
+        from oracle import fastpoisson_oracle as orc
+
+        self._orc = orc
+        self.case = orc.config_case(name, scale)
+        self.threads = threads
+        self.plan = orc.OraclePlan(self.case, workers=threads)
+
+    def solve(self, rhs):
+        return self.plan.solve(rhs)
+
+
+def reference_plan(name, threads, scale=1):
+    """(plan, rhs, kind, label): the reference's own SolverPlan when installed, else the port."""
+    ref = load_reference()
+    if ref is not None:
+        config = build_config(ref, name, scale)
+        t0 = time.perf_counter()
+        plan = ref.SolverPlan(config, threads=threads)
+        plan_s = time.perf_counter() - t0
+        return plan, host_rhs(name, config), "reference", plan_s, "fastpoisson.SolverPlan.solve (baseline/_ref, unmodified)"
+    import paper_1409_8116_b200 as fp
+
+    config = build_config(fp, name, scale)
+    t0 = time.perf_counter()
+    plan = _PortPlan(name, scale, threads)
+    plan_s = time.perf_counter() - t0
+    return plan, host_rhs(name, config), "port", plan_s, "oracle port of the reference algorithm (plan-time arrays built once)"
+
+
+def time_reference(name, threads, reps, warmup, seconds_cap=None, scale=1):
+    plan, rhs, kind, plan_s, label = reference_plan(name, threads, scale)
+    for _ in range(warmup):
+        plan.solve(rhs)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < reps:
+        t0 = time.perf_counter()
+        plan.solve(rhs)
+        times.append(time.perf_counter() - t0)
+        if seconds_cap is not None and time.perf_counter() - t_start > seconds_cap:
+            break
+    return {"times": times, "kind": kind, "plan_s": plan_s, "label": label, "shape": tuple(rhs.shape)}
 
 
 # ------------------------------------------------------------------------------------------
 def run_reference(args, ws, rank):
-    """CPU reference arm: the reference algorithm (oracle port, scipy.fft) on all host cores."""
+    """CPU reference arm: the reference package's own SolverPlan.solve (plan built once,
+    outside the timed steps) on all host cores of rank 0; other ranks exit without work."""
     if rank != 0:
         return
-    from oracle import fastpoisson_oracle as orc
-
-    case = orc.config_case(args.config)
-    rhs = orc.config_rhs(args.config, case, seed=0)
     cores = len(os.sched_getaffinity(0))
-    for _ in range(args.warmup):
-        orc.solve(case, rhs, workers=cores)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        orc.solve(case, rhs, workers=cores)
-    dt = time.perf_counter() - t0
-    value = args.steps / dt
-    n_pts = int(np.prod(case.shape))
+    scale = CPU_PROXY.get(args.config, 1)
+    r = time_reference(args.config, cores, args.steps, args.warmup, scale=scale)
+    dt = sum(r["times"])
+    value = len(r["times"]) / dt
+    n_pts = int(np.prod(r["shape"]))
+    proxy = f" (labelled proxy {r['shape']}: the full grid needs ~270 GB host RAM)" if scale != 1 else ""
+    t1 = None
+    if not args.no_t1:
+        r1 = time_reference(args.config, 1, 1, 0, scale=scale)
+        t1 = {"value": 1.0 / statistics.median(r1["times"]), "unit": "solves/s", "cores": 1,
+              "sample": f"{len(r1['times'])} solve(s), threads=1, after the T=all run warmed the process"}
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": case.dtype.name,
-        "data": "synthetic (seeded N(0,1), mean removed)",
-        "config": {"workload": WORKLOADS[args.config], "grid": list(case.shape)},
+        "steps": len(r["times"]), "warmup": args.warmup, "ms_per_step": dt / len(r["times"]) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if BENCH_CONFIGS[args.config][2] == "single" else "f64",
+        "data": "synthetic (seeded N(0,1), BASELINE.json distributions)",
+        "config": {"workload": WORKLOADS[args.config] + proxy, "grid": list(r["shape"])},
         "gpoints_per_s": value * n_pts / 1e9,
-        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full {args.config} solves after {args.warmup} warm-up; "
-                                   "oracle/fastpoisson_oracle.solve (reference algorithm, scipy.fft workers=all cores)"},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": r["kind"],
+                         "sample": f"{len(r['times'])} full solves after {args.warmup} warm-up, plan built once "
+                                   f"({r['plan_s']:.2f} s, untimed); {r['label']}, threads={cores}{proxy}",
+                         "plan_s": r["plan_s"], "median_s": statistics.median(r["times"]), "t1": t1},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample(name, seconds_cap=30.0):
-    from oracle import fastpoisson_oracle as orc
-
-    case = orc.config_case(name)
-    rhs = orc.config_rhs(name, case, seed=0)
+def cpu_baseline_sample(name, seconds_cap=30.0, with_t1=True):
+    """Bounded CPU sample for the GPU line: the reference's SolverPlan.solve on all
+    host cores (median of <= 3 after 1 warm-up), plus one single-thread solve."""
     cores = len(os.sched_getaffinity(0))
-    orc.solve(case, rhs, workers=cores)  # warm-up
-    times = []
-    t_start = time.perf_counter()
-    while len(times) < 3 and (time.perf_counter() - t_start) < seconds_cap:
-        t0 = time.perf_counter()
-        orc.solve(case, rhs, workers=cores)
-        times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    return {"value": 1.0 / med, "unit": "solves/s", "cores": cores, "kind": "port",
-            "sample": f"median of {len(times)} full {name} solves after 1 warm-up; oracle port of the reference "
-                      "algorithm (scipy.fft, workers=all cores) on this box's host"}
+    scale = CPU_PROXY.get(name, 1)
+    r = time_reference(name, cores, 3, 1, seconds_cap=seconds_cap, scale=scale)
+    med = statistics.median(r["times"])
+    proxy = f"; labelled proxy grid {r['shape']} (full grid needs ~270 GB host RAM)" if scale != 1 else ""
+    out = {"value": 1.0 / med, "unit": "solves/s", "cores": cores, "kind": r["kind"],
+           "sample": f"median of {len(r['times'])} full {name} solves after 1 warm-up, plan built once "
+                     f"({r['plan_s']:.2f} s, untimed); {r['label']}, threads={cores}{proxy}",
+           "grid": list(r["shape"])}
+    if scale != 1:
+        out["gpoints_per_s"] = float(np.prod(r["shape"])) / med / 1e9
+    if with_t1:
+        r1 = time_reference(name, 1, 1, 0, scale=scale)
+        out["t1"] = {"value": 1.0 / r1["times"][0], "unit": "solves/s", "cores": 1,
+                     "sample": "one solve, threads=1"}
+    return out
+
+
+def measure_pcie(dev, nbytes=1 << 30, reps=3):
+    """Pinned host <-> device copy rates (GB/s): each direction alone and both at once
+    on two streams (PCIe is full duplex) -- the roofline of the e2e number."""
+    import torch
+
+    h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    cur = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(reps):
+            fn()
+        e1.record(cur)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps * 1e-3
+
+    def both():
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d_a.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_b, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    t_in = timed(lambda: d_a.copy_(h_in, non_blocking=True))
+    t_out = timed(lambda: h_out.copy_(d_b, non_blocking=True))
+    t_both = timed(both)
+    del h_in, h_out, d_a, d_b
+    return {"h2d_gbs": nbytes / t_in / 1e9, "d2h_gbs": nbytes / t_out / 1e9,
+            "duplex_gbs_each_way": nbytes / t_both / 1e9,
+            "how": f"pinned {nbytes >> 20} MiB copies, CUDA events, mean of {reps}; duplex = both directions "
+                   "at once on two streams"}
 
 
 def measure_e2e(plan, rhs, shape, tdt, n_pts, s, args, ws, dist, dev):
@@ -200,8 +363,15 @@ def measure_e2e(plan, rhs, shape, tdt, n_pts, s, args, ws, dist, dev):
         tt = torch.tensor([batch_dt, single_dt], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         batch_dt, single_dt = float(tt[0]), float(tt[1])
-    return {"value": ws * e2e_steps / batch_dt, "unit": "solves/s", "h2d_bytes_per_step": n_pts * s,
-            "d2h_bytes_per_step": n_pts * s + 16,
+    pcie = measure_pcie(dev)
+    # PCIe roofline of a streamed solve: H2D and D2H overlap (full duplex), so a step
+    # costs at least max(bytes_in, bytes_out) / duplex rate
+    bound = max(n_pts * s, n_pts * s + 16) / (pcie["duplex_gbs_each_way"] * 1e9)
+    value = ws * e2e_steps / batch_dt
+    pcie["roofline_solves_per_s"] = ws / bound
+    pcie["frac"] = value / pcie["roofline_solves_per_s"]
+    return {"value": value, "unit": "solves/s", "h2d_bytes_per_step": n_pts * s,
+            "d2h_bytes_per_step": n_pts * s + 16, "pcie": pcie, "pcie_frac": pcie["frac"],
             "path": "SolverPlan.solve_batch(pinned numpy rhs per step -> pinned numpy out per step)",
             "single_call": {"value": ws * e2e_steps / single_dt, "unit": "solves/s",
                             "path": "SolverPlan.solve(pinned numpy rhs, out=pinned numpy) once per step"}}
@@ -216,6 +386,10 @@ def run_dist(args, ws, rank, local):
     from paper_1409_8116_b200 import _device as dv
     from paper_1409_8116_b200.distributed import DistributedSolverPlan
 
+    # NCCL init lines (rank count, transport: NVLink / NVLS) on stderr, away from the JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -350,7 +524,7 @@ def run_ours(args, ws, rank, local):
         arr = (ctypes.c_void_p * k)()
         for i in range(k):
             h = ctypes.c_void_p()
-            nat.check(lib.fp_event_create(ctypes.byref(h)))
+            nat.check(lib.fp_event_create_on(local, ctypes.byref(h)))
             arr[i] = h
         return arr
 
@@ -498,9 +672,23 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-t1", action="store_true", help="reference arm: skip the single-thread timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched without torchrun: start the N ranks ourselves (one process per GPU)
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if args.gpus != ws:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return

@@ -16,6 +16,10 @@
  *   fp_plan_workspace_bytes  per-call workspace of solve  solver.py:213 (work copy)
  *   fp_solve            SolverPlan.solve (device buffers, async)  solver.py:191-230
  *   fp_solve_ex         same, with per-kernel CUDA events (bench / profiling)
+ *   fp_solve_override   same, dividing by the caller's dense `_inv_lam` table instead
+ *                       of the plan's eigenvalues (SolverPlan._inv_lam mutated for
+ *                       fault injection, verifysuite.py:83-88; solver.py:151-159,221)
+ *   fp_plan_spectrum    extents of that table (the half spectrum)  solver.py:147-159
  *   fp_solve_host       SolverPlan.solve (host buffers, sync)     solver.py:191-230
  *   fp_removed_mean     SolveReport.removed_mean        solver.py:218-220
  *   fp_transform_create TransformPlan(kind, n)          transforms.py:128-146
@@ -135,6 +139,12 @@ FP_API fp_status fp_plan_info_get(const fp_plan* plan, fp_plan_info* info);
 /* out_dense != 0: the caller promises `out` is a dense C-order array that the
  * solve may use as its real-valued scratch (smaller workspace). */
 FP_API fp_status fp_plan_workspace_bytes(const fp_plan* plan, int out_dense, size_t* bytes);
+/* same, for fp_solve_override when inv_lam_override != 0 */
+FP_API fp_status fp_plan_workspace_bytes_ex(const fp_plan* plan, int out_dense, int inv_lam_override,
+                                            size_t* bytes);
+/* Spectral extents of the solve's middle state (ext[a] = n[a], except the real-FFT
+ * periodic axis r_axis: n/2 + 1; r_axis = -1 when no axis is periodic). */
+FP_API fp_status fp_plan_spectrum(const fp_plan* plan, int64_t ext[3], int* r_axis);
 
 /* Asynchronous device solve.  rhs_dtype: FP_F64 or FP_F32 (cast on load);
  * out has the plan precision.  dev_info: device memory (zeroed by the call).
@@ -155,6 +165,19 @@ FP_API fp_status fp_solve_ex(const fp_plan* plan,
                              void* workspace, size_t workspace_bytes,
                              void* stream, fp_solve_info* dev_info,
                              void* const* phase_events, void* const* pass_events);
+
+/* fp_solve with the reference's dense diagonal: inv_lam is device memory in the
+ * plan precision, C order over fp_plan_spectrum's extents, holding
+ * backward_scale / lambda (0 on null modes) at every half-spectrum index --
+ * for periodic axes the Hermitian average (f(k) + f(-k)) / 2 of the full
+ * table, which is what `.real` of the inverse FFT keeps (solver.py:245-246).
+ * The middle axis then runs as forward pass + scale + inverse pass. */
+FP_API fp_status fp_solve_override(const fp_plan* plan,
+                                   const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                                   void* out, const int64_t* out_strides,
+                                   void* workspace, size_t workspace_bytes,
+                                   void* stream, fp_solve_info* dev_info,
+                                   void* const* phase_events, const void* inv_lam);
 
 /* Synchronous host-buffer solve (H2D, fp_solve, D2H); returns FP_ERR_NONFINITE
  * without touching `out` when rhs holds NaN/Inf. */
@@ -231,7 +254,9 @@ FP_API fp_status fp_solve_phase(const fp_plan* plan, int phase,
                                 fp_solve_info* dev_info);
 
 /* CUDA event helpers for SolveReport.timing (phase_events of fp_solve). */
-FP_API fp_status fp_event_create(void** event);
+FP_API fp_status fp_event_create(void** event);      /* on the current device */
+/* same, on `device` (events must live on the device of the stream they are recorded on) */
+FP_API fp_status fp_event_create_on(int device, void** event);
 FP_API fp_status fp_event_destroy(void* event);
 FP_API fp_status fp_event_elapsed_ms(void* start, void* stop, float* ms);
 

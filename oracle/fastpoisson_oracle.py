@@ -393,51 +393,72 @@ _EXTENDED_LIMIT = 4096  # solver.py:53
 _HAVE_EXTENDED = np.finfo(np.longdouble).eps < np.finfo(np.float64).eps
 
 
+class OraclePlan:
+    """Plan-time half of SolverPlan (solver.py:136-181): the dense combined
+    eigenvalues and their inverse (eigenvalues.py:94-114, solver.py:149-159),
+    built once; ``solve`` is the per-call half (solver.py:191-249)."""
+
+    def __init__(self, case: Case, workers=None, extended=True):
+        self.case = case
+        self.workers = workers
+        shape = case.shape
+        dtype = case.dtype
+        work_dtype = dtype
+        if extended and math.prod(shape) <= _EXTENDED_LIMIT and _HAVE_EXTENDED and dtype == np.float64:
+            work_dtype = np.dtype(np.longdouble)
+        self.work_dtype = work_dtype
+        d = len(shape)
+        lam = np.zeros(shape, dtype=np.float64)
+        for ax, a in enumerate(case.axes):
+            s = [1] * d
+            s[ax] = a.n
+            lam += eigenvalues(a, case.approx).reshape(s)
+        bscale = math.prod(backward_scale(a) for a in case.axes)
+        inv = np.zeros_like(lam)
+        np.divide(bscale, lam, out=inv, where=lam != 0.0)
+        self.inv = inv.astype(work_dtype)
+
+    def solve(self, rhs):
+        """Return (solution, removed_mean) exactly as SolverPlan.solve computes them."""
+        case, workers, work_dtype = self.case, self.workers, self.work_dtype
+        shape = case.shape
+        rhs = np.asarray(rhs)
+        if rhs.shape != shape:
+            raise ValueError("rhs extents do not match")
+        if not np.isfinite(rhs).all():
+            raise ValueError("rhs contains non-finite values")
+        d = len(shape)
+        periodic = case.periodic_axes
+        real_axes = tuple(i for i in range(d) if i not in periodic)
+        work = np.array(rhs, dtype=work_dtype, copy=True, order="C")
+        for ax in real_axes:
+            work = forward_1d(pair(case.axes[ax])[0], work, axis=ax, workers=workers)
+        if periodic:
+            scale = math.prod(shape[ax] for ax in periodic)
+            work = sfft.fftn(work, axes=periodic, workers=workers) / scale
+        removed_mean = 0.0
+        if case.singular:
+            null_scale = math.prod(null_coeff(a) for a in case.axes)
+            removed_mean = float(np.real(work[(0,) * d])) / null_scale
+        work *= self.inv
+        if periodic:
+            scale = math.prod(shape[ax] for ax in periodic)
+            work = sfft.ifftn(work, axes=periodic, workers=workers) * scale
+            work = np.ascontiguousarray(work.real, dtype=work_dtype)
+        for ax in reversed(real_axes):
+            work = backward_1d(pair(case.axes[ax])[1], work, axis=ax, workers=workers)
+        if case.singular:
+            work -= work.mean()
+        return np.asarray(work, dtype=case.dtype), removed_mean
+
+
 def solve(case: Case, rhs, workers=None, extended=True):
-    """Return (solution, removed_mean) exactly as SolverPlan.solve computes them."""
-    shape = case.shape
+    """Return (solution, removed_mean) exactly as SolverPlan.solve computes them
+    (plan and solve in one call; see OraclePlan)."""
     rhs = np.asarray(rhs)
-    if rhs.shape != shape:
+    if rhs.shape != case.shape:
         raise ValueError("rhs extents do not match")
-    if not np.isfinite(rhs).all():
-        raise ValueError("rhs contains non-finite values")
-    dtype = case.dtype
-    work_dtype = dtype
-    if extended and math.prod(shape) <= _EXTENDED_LIMIT and _HAVE_EXTENDED and dtype == np.float64:
-        work_dtype = np.dtype(np.longdouble)
-    # dense combined eigenvalues and inverse (eigenvalues.py:94-114, solver.py:149-159)
-    d = len(shape)
-    lam = np.zeros(shape, dtype=np.float64)
-    for ax, a in enumerate(case.axes):
-        s = [1] * d
-        s[ax] = a.n
-        lam += eigenvalues(a, case.approx).reshape(s)
-    bscale = math.prod(backward_scale(a) for a in case.axes)
-    inv = np.zeros_like(lam)
-    np.divide(bscale, lam, out=inv, where=lam != 0.0)
-    inv = inv.astype(work_dtype)
-    periodic = case.periodic_axes
-    real_axes = tuple(i for i in range(d) if i not in periodic)
-    work = np.array(rhs, dtype=work_dtype, copy=True, order="C")
-    for ax in real_axes:
-        work = forward_1d(pair(case.axes[ax])[0], work, axis=ax, workers=workers)
-    if periodic:
-        scale = math.prod(shape[ax] for ax in periodic)
-        work = sfft.fftn(work, axes=periodic, workers=workers) / scale
-    removed_mean = 0.0
-    if case.singular:
-        null_scale = math.prod(null_coeff(a) for a in case.axes)
-        removed_mean = float(np.real(work[(0,) * d])) / null_scale
-    work *= inv
-    if periodic:
-        scale = math.prod(shape[ax] for ax in periodic)
-        work = sfft.ifftn(work, axes=periodic, workers=workers) * scale
-        work = np.ascontiguousarray(work.real, dtype=work_dtype)
-    for ax in reversed(real_axes):
-        work = backward_1d(pair(case.axes[ax])[1], work, axis=ax, workers=workers)
-    if case.singular:
-        work -= work.mean()
-    return np.asarray(work, dtype=dtype), removed_mean
+    return OraclePlan(case, workers, extended).solve(rhs)
 
 
 # -- solver.py:286-338 -----------------------------------------------------------

@@ -91,6 +91,13 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_size_t,
          c_void_p, c_void_p, POINTER(c_void_p), POINTER(c_void_p)],
     ),
+    "fp_solve_override": (
+        c_int,
+        [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_size_t,
+         c_void_p, c_void_p, POINTER(c_void_p), c_void_p],
+    ),
+    "fp_plan_workspace_bytes_ex": (c_int, [c_void_p, c_int, c_int, POINTER(c_size_t)]),
+    "fp_plan_spectrum": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int)]),
     "fp_solve_host": (
         c_int,
         [c_void_p, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), POINTER(FpSolveResult)],
@@ -120,6 +127,7 @@ SIGNATURES = {
          c_size_t, c_void_p, c_void_p],
     ),
     "fp_event_create": (c_int, [POINTER(c_void_p)]),
+    "fp_event_create_on": (c_int, [c_int, POINTER(c_void_p)]),
     "fp_event_destroy": (c_int, [c_void_p]),
     "fp_event_elapsed_ms": (c_int, [c_void_p, c_void_p, POINTER(c_float)]),
 }

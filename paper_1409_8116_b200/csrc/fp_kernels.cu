@@ -300,9 +300,16 @@ __global__ void scale_kernel(const ScalePass p) {
         const long long k1 = r % p.ext[1];
         const long long k0 = r / p.ext[1];
         const long long ks[3] = {k0, k1, k2};
-        double lam = 0.0;
-        for (int a = 0; a < p.ndim; ++a) lam += p.lam[a][ks[3 - p.ndim + a]];
-        const double f = lam != 0.0 ? (p.bscale / lam) * p.inv_np : 0.0;
+        double f;
+        if (p.ovr) {
+            // dense _inv_lam override (solver.py:221 `work *= _inv_lam`): the table already
+            // carries bscale / lambda and its zeros; only the DFT normalisation is added
+            f = (double)reinterpret_cast<const T*>(p.ovr)[idx] * p.inv_np;
+        } else {
+            double lam = 0.0;
+            for (int a = 0; a < p.ndim; ++a) lam += p.lam[a][ks[3 - p.ndim + a]];
+            f = lam != 0.0 ? (p.bscale / lam) * p.inv_np : 0.0;
+        }
         const long long off = k0 * p.st[0] + k1 * p.st[1] + k2 * p.st[2];
         if (cpx) {
             cx<T>* d = reinterpret_cast<cx<T>*>(p.data) + off;

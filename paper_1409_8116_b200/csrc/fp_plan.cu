@@ -126,6 +126,8 @@ struct fp_plan {
     double np_prod = 1.0;
     double null_scale = 1.0;
     std::vector<PassT> passes;
+    std::vector<PassT> passes_ovr;   // middle axis split around a dense _inv_lam scale (override solves)
+    bool need_cw_ovr = false;
     DevTables tab[3];
     double* d_lam[3] = {nullptr, nullptr, nullptr};       // per-axis eigenvalue tables
     double* d_lam_pad[3] = {nullptr, nullptr, nullptr};   // the same, from the leading pad entry
@@ -699,6 +701,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
     const double inv_np = 1.0 / P->np_prod;
     bool complex_state = false;
     int cur = B_RHS;
+    bool rs_dummy = false;
     const int realbuf = B_RS;  // resolved at solve time to OUT when out is dense
 
     auto make_fft = [&](int t, int op, bool in_cpx, bool out_cpx, int in_buf, int out_buf, int phase) {
@@ -803,6 +806,9 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         return ps;
     };
 
+    auto schedule = [&](bool split, std::vector<PassT>& L, bool& need_cw) {
+    complex_state = false;
+    cur = B_RHS;
     const bool only_middle = order.size() == 1;
     // forward passes
     for (size_t i = 0; i + 1 < order.size(); ++i) {
@@ -812,9 +818,9 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         const bool out_cpx = complex_state || rf;
         int dst = out_cpx ? B_CW : realbuf;
         if (dist && i + 2 == order.size()) dst = B_X;   // pack for the all-to-all
-        else if (out_cpx) P->need_cw = true; else P->need_rs = true;
-        if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_FWD, in_cpx, out_cpx, cur, dst, 0));
-        else P->passes.push_back(make_dense(t, true, in_cpx, out_cpx, cur, dst, 0));
+        else if (out_cpx) need_cw = true; else rs_dummy = true;
+        if (Mx[t] > 0) L.push_back(make_fft(t, OP_FWD, in_cpx, out_cpx, cur, dst, 0));
+        else L.push_back(make_dense(t, true, in_cpx, out_cpx, cur, dst, 0));
         if (rf) complex_state = true;
         cur = dst;
     }
@@ -823,16 +829,29 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         const int t = P->middle;
         const bool rf = t == P->r_axis;
         const int dst = only_middle ? B_OUT : cur;
-        if (dist) {
+        if (split) {
+            // _inv_lam override (SolverPlan._inv_lam written by the caller, verifysuite.py:83-88):
+            // forward along the middle axis, the stand-alone scale reading the caller's dense
+            // factor table, inverse -- the reference's `work *= _inv_lam` (solver.py:221)
+            const bool in_c = complex_state, mid_c = complex_state || rf;
+            int work = cur;
+            if (only_middle || rf) work = mid_c ? B_CW : realbuf;
+            if (mid_c && work == B_CW) need_cw = true;
+            if (Mx[t] > 0) L.push_back(make_fft(t, OP_FWD, in_c, mid_c, cur, work, 1));
+            else L.push_back(make_dense(t, true, in_c, mid_c, cur, work, 1));
+            L.push_back(make_scale(1, work, mid_c));
+            if (Mx[t] > 0) L.push_back(make_fft(t, OP_INV, mid_c, in_c, work, dst, 1));
+            else L.push_back(make_dense(t, false, mid_c, in_c, work, dst, 1));
+        } else if (dist) {
             // MID over the receive layout: global axis 0 in P blocks of a0 planes
             PassT mid = make_fft(t, OP_MID, complex_state, complex_state, B_X, B_X, 1);
             mid.dist_mid = true;
             if (d == 3) { mid.fp.g.na = (int)DL.B; mid.fp.g.nb = (int)DL.e2; }
             else { mid.fp.g.na = 1; mid.fp.g.nb = (int)DL.B; }
             fft_tile_shape(mid.fp, P->f32, complex_state, mid.fp.g.na, mid.fp.g.nb);
-            P->passes.push_back(mid);
+            L.push_back(mid);
         } else if (Mx[t] > 0) {
-            P->passes.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
+            L.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
         } else if (P->tab[t].mr && mr_mid_fits(P->tab[t], cfg->n[t], P->f32)) {
             // mixed-radix MID: forward, eigenvalue scale, inverse on the tile
             PassT ps{};
@@ -856,24 +875,24 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             sc.bscale = P->bscale;
             sc.inv_np = inv_np;
             sc.singular = P->singular;
-            P->passes.push_back(ps);
+            L.push_back(ps);
         } else if (!rf) {
             // dense forward, scale, dense inverse on the same buffer
             int work = cur;
             if (only_middle) work = complex_state ? B_CW : realbuf;
-            if (only_middle && !complex_state) P->need_rs = true;
-            P->passes.push_back(make_dense(t, true, complex_state, complex_state, cur, work, 1));
-            P->passes.push_back(make_scale(1, work, complex_state));
-            P->passes.push_back(make_dense(t, false, complex_state, complex_state, work, dst, 1));
+            if (only_middle && !complex_state) rs_dummy = true;
+            L.push_back(make_dense(t, true, complex_state, complex_state, cur, work, 1));
+            L.push_back(make_scale(1, work, complex_state));
+            L.push_back(make_dense(t, false, complex_state, complex_state, work, dst, 1));
         } else {
             // real-FFT middle axis on the dense engine: real -> half spectrum -> real
-            P->need_cw = true;
-            P->passes.push_back(make_dense(t, true, false, true, cur, B_CW, 1));
+            need_cw = true;
+            L.push_back(make_dense(t, true, false, true, cur, B_CW, 1));
             complex_state = true;
-            P->passes.push_back(make_scale(1, B_CW, true));
+            L.push_back(make_scale(1, B_CW, true));
             // the inverse writes real data: extents of other axes unchanged
             PassT inv = make_dense(t, false, true, false, B_CW, dst, 1);
-            P->passes.push_back(inv);
+            L.push_back(inv);
             complex_state = false;
         }
     }
@@ -886,13 +905,16 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         const bool last = i == 0;
         int dst = last ? B_OUT : (out_cpx ? B_CW : (in_cpx ? realbuf : cur));
         if (!last && cur == B_X) dst = out_cpx ? B_CW : realbuf;   // unpack out of the exchange buffer
-        if (!out_cpx && !last) P->need_rs = true;
-        if (out_cpx && !last) P->need_cw = true;
-        if (Mx[t] > 0) P->passes.push_back(make_fft(t, OP_INV, in_cpx, out_cpx, cur, dst, 2));
-        else P->passes.push_back(make_dense(t, false, in_cpx, out_cpx, cur, dst, 2));
+        if (!out_cpx && !last) rs_dummy = true;
+        if (out_cpx && !last) need_cw = true;
+        if (Mx[t] > 0) L.push_back(make_fft(t, OP_INV, in_cpx, out_cpx, cur, dst, 2));
+        else L.push_back(make_dense(t, false, in_cpx, out_cpx, cur, dst, 2));
         if (rf) complex_state = false;
         cur = dst;
     }
+    };
+    schedule(false, P->passes, P->need_cw);
+    if (!dist) schedule(true, P->passes_ovr, P->need_cw_ovr);
     // the first pass checks finiteness of the rhs (solver.py:201-202)
     *out = P;
     return FP_OK;
@@ -922,8 +944,8 @@ FP_API fp_status fp_plan_info_get(const fp_plan* P, fp_plan_info* info) {
 
 static size_t align_up(size_t x) { return (x + 255) / 256 * 256; }
 
-static size_t cw_bytes(const fp_plan* P) {
-    if (!P->need_cw) return 0;
+static size_t cw_bytes(const fp_plan* P, bool ovr = false) {
+    if (!(ovr ? P->need_cw_ovr : P->need_cw)) return 0;
     size_t cnt = 1;
     for (int a = 0; a < P->ndim - 1; ++a) cnt *= (size_t)P->cext[a];
     cnt *= (size_t)P->cpitch_last;
@@ -940,8 +962,12 @@ static size_t mean_bytes(const fp_plan* P) {
 }
 
 FP_API fp_status fp_plan_workspace_bytes(const fp_plan* P, int out_dense, size_t* bytes) {
+    return fp_plan_workspace_bytes_ex(P, out_dense, 0, bytes);
+}
+
+FP_API fp_status fp_plan_workspace_bytes_ex(const fp_plan* P, int out_dense, int inv_lam_override, size_t* bytes) {
     if (!P || !bytes) return fail(FP_ERR_VALUE, "NULL argument");
-    size_t b = cw_bytes(P);
+    size_t b = cw_bytes(P, inv_lam_override != 0);
     // with a strided `out` the real scratch (also the dtype-cast target) lives here
     if (!out_dense) b += rs_bytes(P);
     b += mean_bytes(P);
@@ -971,8 +997,10 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
                             void* const* pass_events, void* xbuf, int ph_lo, int ph_hi,
-                            const Producer* prod = nullptr) {
+                            const Producer* prod = nullptr, const void* ovr = nullptr) {
     if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
+    if (ovr && P->passes_ovr.empty()) return fail(FP_ERR_UNSUPPORTED, "_inv_lam override: single-GPU plans only");
+    const std::vector<PassT>& PL = ovr ? P->passes_ovr : P->passes;
     const bool need_rhs = ph_lo == 0, need_out = ph_hi == 2;
     if ((need_rhs && !rhs) || (need_out && !out)) return fail(FP_ERR_VALUE, "rhs/out is NULL");
     if (P->nranks > 1 && !xbuf) return fail(FP_ERR_VALUE, "distributed plan: exchange buffer is NULL");
@@ -992,7 +1020,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
     bool out_dense = true;
     for (int a = 0; a < d; ++a) if (P->n[a] > 1 && os_s[a] != dense_r[a]) out_dense = false;
     size_t need = 0;
-    fp_plan_workspace_bytes(P, out_dense, &need);
+    fp_plan_workspace_bytes_ex(P, out_dense, ovr != nullptr, &need);
     if (need > 0 && (!workspace || workspace_bytes < need))
         return fail(FP_ERR_VALUE, "workspace too small: need " + std::to_string(need) + " bytes");
     DeviceGuard dg(P->device);
@@ -1000,7 +1028,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
     if (dev_info && ph_lo == 0) CUDA_TRY(cudaMemsetAsync(dev_info, 0, sizeof(fp_solve_info), st));
 
     void* cw = workspace;
-    void* rsb = out_dense ? out : (void*)((char*)workspace + cw_bytes(P));
+    void* rsb = out_dense ? out : (void*)((char*)workspace + cw_bytes(P, ovr != nullptr));
     // rhs in another precision: cast once into the real scratch (dense, plan-typed)
     const int plan_fp = P->f32 ? FP_F32 : FP_F64;
     if (rhs_dtype != plan_fp && ph_lo == 0) {
@@ -1019,7 +1047,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
     // divergence kernel fills the (dense) real scratch and the solve reads that
     bool prod_in_pass = false;
     if (prod && ph_lo == 0) {
-        const PassT& F = P->passes[0];
+        const PassT& F = PL[0];
         prod_in_pass = F.engine == EN_FFT && F.fp.op == OP_FWD && F.fp.family == FAM_CONTIG && F.t == d - 1 &&
                        (F.fp.fkind == FK_DCT2 || F.fp.fkind == FK_RFFT);
         if (!prod_in_pass) {
@@ -1061,8 +1089,8 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], st));
     int phase = 0;
     bool first = true;
-    for (size_t i = 0; i < P->passes.size(); ++i) {
-        const PassT& T = P->passes[i];
+    for (size_t i = 0; i < PL.size(); ++i) {
+        const PassT& T = PL[i];
         if (T.phase < ph_lo || T.phase > ph_hi) continue;
         while (ev && phase < T.phase) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
         if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[i], st));
@@ -1136,6 +1164,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                 p.st[3 - d + a] = si[a];
             }
             p.dc_out = dev_info ? &dev_info->dc : nullptr;
+            p.ovr = ovr;
             e = launch_scale_pass(p, P->f32, st);
         }
         if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
@@ -1150,7 +1179,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
         cudaError_t e = launch_mean_pass(m, P->f32, st);
         if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("mean removal launch failed: ") + cudaGetErrorString(e));
     }
-    if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[P->passes.size()], st));
+    if (pass_events) CUDA_TRY(cudaEventRecord((cudaEvent_t)pass_events[PL.size()], st));
     while (ev && phase < 3) { ++phase; CUDA_TRY(cudaEventRecord(ev[phase], st)); }
     return FP_OK;
 }
@@ -1162,6 +1191,23 @@ FP_API fp_status fp_solve_ex(const fp_plan* P, const void* rhs, int rhs_dtype, c
     if (P && P->nranks > 1) return fail(FP_ERR_VALUE, "distributed plan: use fp_solve_phase");
     return solve_impl(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
                       dev_info, phase_events, pass_events, nullptr, 0, 2);
+}
+
+FP_API fp_status fp_solve_override(const fp_plan* P, const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
+                                   void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
+                                   void* stream, fp_solve_info* dev_info, void* const* phase_events,
+                                   const void* inv_lam) {
+    if (P && P->nranks > 1) return fail(FP_ERR_UNSUPPORTED, "_inv_lam override: single-GPU plans only");
+    if (!inv_lam) return fail(FP_ERR_VALUE, "inv_lam is NULL");
+    return solve_impl(P, rhs, rhs_dtype, rhs_strides, out, out_strides, workspace, workspace_bytes, stream,
+                      dev_info, phase_events, nullptr, nullptr, 0, 2, nullptr, inv_lam);
+}
+
+FP_API fp_status fp_plan_spectrum(const fp_plan* P, int64_t ext[3], int* r_axis) {
+    if (!P || !ext || !r_axis) return fail(FP_ERR_VALUE, "NULL argument");
+    for (int a = 0; a < 3; ++a) ext[a] = a < P->ndim ? P->cext[a] : 1;
+    *r_axis = P->r_axis;
+    return FP_OK;
 }
 
 FP_API fp_status fp_solve_phase(const fp_plan* P, int phase, const void* rhs, int rhs_dtype,
@@ -1506,6 +1552,15 @@ FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int
 
 FP_API fp_status fp_event_create(void** event) {
     if (!event) return fail(FP_ERR_VALUE, "NULL argument");
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    *event = (void*)e;
+    return FP_OK;
+}
+
+FP_API fp_status fp_event_create_on(int device, void** event) {
+    if (!event) return fail(FP_ERR_VALUE, "NULL argument");
+    DeviceGuard dg(device);
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreate(&e));
     *event = (void*)e;

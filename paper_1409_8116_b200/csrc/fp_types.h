@@ -173,6 +173,7 @@ struct ScalePass {              // stand-alone eigenvalue scale (dense middle)
     double inv_np;
     int singular;
     double* dc_out;
+    const void* ovr;            // NULL, or the caller's dense factor table (plan precision, C order over ext)
 };
 
 struct MeanPass {               // subtract the arithmetic mean (DCT-I plans)

@@ -133,14 +133,16 @@ class SolveReport:
 
 
 class _Events:
-    """Four CUDA events (start / after forward / after diagonal / end)."""
+    """Four CUDA events (start / after forward / after diagonal / end), created on
+    the plan's device (an event must share the device of the stream it is
+    recorded on, whatever device is current)."""
 
-    def __init__(self, lib):
+    def __init__(self, lib, device_index: int):
         self._lib = lib
         self.ev = (ctypes.c_void_p * 4)()
         for i in range(4):
             h = ctypes.c_void_p()
-            nat.check(lib.fp_event_create(ctypes.byref(h)))
+            nat.check(lib.fp_event_create_on(int(device_index), ctypes.byref(h)))
             self.ev[i] = h
 
     def timing(self) -> dict:
@@ -192,6 +194,9 @@ class SolverPlan:
         if config.singular:
             self._null_scale = math.prod(_ONES_NULL_COEFF[p.forward](g.n) for g, p in zip(config.grids, self._pairs))
         self._inv_lam_cache = None
+        self._inv_lam_pristine = None
+        self._ovr_src = None
+        self._ovr_dev = None
         self._device = dv.require_cuda(device)
         self._lib = nat.load()
         self._handle = self._create_native()
@@ -246,17 +251,66 @@ class SolverPlan:
     def _inv_lam(self) -> np.ndarray:
         """Dense backward_scale / lambda array (solver.py:151-159), built lazily on the host.
 
-        The device never reads it: the middle pass evaluates the same factor
-        from the per-axis tables.  Exposed for API compatibility only.
+        The normal solve never reads it: the middle pass evaluates the same
+        factor from the per-axis tables.  It is writable, as in the reference:
+        once a caller changes it (fault injection, verifysuite.py:83-88), every
+        later solve divides by the caller's table instead (fp_solve_override),
+        exactly like the reference's ``work *= self._inv_lam`` (solver.py:221).
         """
         if self._inv_lam_cache is None:
             lam = combine_eigenvalues(self.tables).values
             inv = np.zeros_like(lam)
             np.divide(self._backward_scale, lam, out=inv, where=lam != 0.0)
             inv = inv.astype(self.dtype)
-            inv.setflags(write=False)
+            self._inv_lam_pristine = inv.copy()
             self._inv_lam_cache = inv
+            self._ovr_src = None
+            self._ovr_dev = None
         return self._inv_lam_cache
+
+    @_inv_lam.setter
+    def _inv_lam(self, value):
+        arr = np.array(value, dtype=self.dtype)
+        if arr.shape != self.shape:
+            raise ValueError(f"_inv_lam must have the plan extents {self.shape}, got {arr.shape}")
+        self._inv_lam  # noqa: B018  (materialize the pristine copy)
+        self._inv_lam_cache = arr
+
+    def _override_table(self):
+        """Device table for fp_solve_override, or None while ``_inv_lam`` is pristine.
+
+        The host array is compared with the pristine copy only after a caller
+        has touched ``_inv_lam``; the half-spectrum table is rebuilt and
+        uploaded only when the array changed since the last upload."""
+        cache = self._inv_lam_cache
+        if cache is None:
+            return None
+        if self._ovr_src is not None and np.array_equal(cache, self._ovr_src):
+            return self._ovr_dev
+        if np.array_equal(cache, self._inv_lam_pristine):
+            self._ovr_src, self._ovr_dev = None, None
+            return None
+        ext = (ctypes.c_int64 * 3)()
+        r_axis = ctypes.c_int()
+        nat.check(self._lib.fp_plan_spectrum(self._handle, ext, ctypes.byref(r_axis)))
+        table = np.asarray(cache, dtype=np.float64)
+        per = self._periodic_axes
+        if per:
+            # `.real` of the inverse FFT keeps (f(k) + f(-k)) / 2 (the Hermitian part of
+            # the multiplier), which is what a half-spectrum pipeline can apply
+            mirrored = table
+            for ax in per:
+                mirrored = np.roll(np.flip(mirrored, axis=ax), 1, axis=ax)
+            table = 0.5 * (table + mirrored)
+        if r_axis.value >= 0:
+            sl = [slice(None)] * self.config.dims
+            sl[r_axis.value] = slice(0, int(ext[r_axis.value]))
+            table = table[tuple(sl)]
+        t = dv.torch()
+        dev = t.from_numpy(np.ascontiguousarray(table, dtype=self.dtype)).to(self._device)
+        self._ovr_src = np.array(cache, copy=True)
+        self._ovr_dev = dev
+        return dev
 
     def workspace_bytes(self, out_dense: bool = True) -> int:
         b = ctypes.c_size_t()
@@ -286,21 +340,34 @@ class SolverPlan:
         rep.timing = events.timing()
         return rep
 
-    def _launch(self, rhs_t, out_t, info_t, events=None, stream=None):
-        """Enqueue one solve on the current stream (no synchronization)."""
+    def _launch(self, rhs_t, out_t, info_t, events=None, stream=None, workspace=None):
+        """Enqueue one solve on the current stream (no synchronization).  The
+        workspace comes from the caching allocator unless the caller passes one
+        (at least ``workspace_bytes(out_t.is_contiguous())`` bytes)."""
         t = dv.torch()
         out_dense = out_t.is_contiguous()
-        ws_bytes = self.workspace_bytes(out_dense)
-        ws = t.empty(max(ws_bytes, 1), dtype=t.uint8, device=self._device)
+        ovr = self._override_table()
+        if ovr is None:
+            ws_bytes = self.workspace_bytes(out_dense)
+        else:
+            b = ctypes.c_size_t()
+            nat.check(self._lib.fp_plan_workspace_bytes_ex(self._handle, int(bool(out_dense)), 1, ctypes.byref(b)))
+            ws_bytes = int(b.value)
+        if workspace is not None and workspace.numel() >= ws_bytes:
+            ws = workspace
+        else:
+            ws = t.empty(max(ws_bytes, 1), dtype=t.uint8, device=self._device)
         st = stream if stream is not None else dv.stream_handle(self._device)
         ev = events.ev if events is not None else None
-        rc = self._lib.fp_solve(
-            self._handle,
-            rhs_t.data_ptr(), dv.fp_dtype_of_torch(rhs_t.dtype), nat.strides_array(rhs_t.stride()),
-            out_t.data_ptr(), nat.strides_array(out_t.stride()),
-            ws.data_ptr(), ws_bytes, st, info_t.data_ptr(), ev)
-        nat.check(rc)
-        return ws
+        args = (self._handle,
+                rhs_t.data_ptr(), dv.fp_dtype_of_torch(rhs_t.dtype), nat.strides_array(rhs_t.stride()),
+                out_t.data_ptr(), nat.strides_array(out_t.stride()),
+                ws.data_ptr(), ws_bytes, st, info_t.data_ptr(), ev)
+        if ovr is None:
+            nat.check(self._lib.fp_solve(*args))
+            return ws
+        nat.check(self._lib.fp_solve_override(*args, ovr.data_ptr()))
+        return (ws, ovr)
 
     def _prepare_device_inputs(self, rhs_t, out_t):
         t = dv.torch()
@@ -328,7 +395,7 @@ class SolverPlan:
         t = dv.torch()
         rhs_t, out_t = self._prepare_device_inputs(rhs_t, out_t)
         info_t = t.zeros(16, dtype=t.uint8, device=self._device)
-        events = _Events(self._lib)
+        events = _Events(self._lib, self._device.index)
         ws = self._launch(rhs_t, out_t, info_t, events)
         info_host = nat.FpSolveInfo.from_buffer_copy(info_t.cpu().numpy().tobytes())
         del ws
@@ -346,7 +413,7 @@ class SolverPlan:
         rhs_t = dv.to_device(rhs_arr, self._device)
         out_t = t.empty(self.shape, dtype=dv.torch_dtype(self.dtype), device=self._device)
         info_t = t.zeros(16, dtype=t.uint8, device=self._device)
-        events = _Events(self._lib)
+        events = _Events(self._lib, self._device.index)
         ws = self._launch(rhs_t, out_t, info_t, events)
         info_host = nat.FpSolveInfo.from_buffer_copy(info_t.cpu().numpy().tobytes())
         del ws
@@ -390,9 +457,11 @@ class SolverPlan:
         ev_in = [t.cuda.Event() for _ in range(2)]
         ev_run = [t.cuda.Event() for _ in range(2)]
         ev_out = [t.cuda.Event() for _ in range(2)]
-        events = [_Events(self._lib) for _ in rhs_list]
+        events = [_Events(self._lib, self._device.index) for _ in rhs_list]
         host_out = [None] * len(rhs_list)
-        keep = []
+        # one workspace per double buffer, reused in stream order on s_run
+        ws_bytes = self.workspace_bytes(out_dense=True)
+        wss = [t.empty(max(ws_bytes, 1), dtype=t.uint8, device=dev) for _ in range(min(2, len(rhs_list)))]
         for i, r in enumerate(rhs_list):
             b = i & 1
             if r.dtype not in (np.float32, np.float64):
@@ -408,8 +477,7 @@ class SolverPlan:
                 s_run.wait_event(ev_in[b])
                 if i >= 2:
                     s_run.wait_event(ev_out[b])         # d_out[b] drained by the copy of solve i-2
-                ws = self._launch(d_in[b], d_out[b], infos[i], events[i], stream=s_run.cuda_stream)
-                keep.append(ws)
+                self._launch(d_in[b], d_out[b], infos[i], events[i], stream=s_run.cuda_stream, workspace=wss[b])
                 ev_run[b].record(s_run)
             with t.cuda.stream(s_out):
                 s_out.wait_event(ev_run[b])
@@ -431,7 +499,7 @@ class SolverPlan:
             if host_out[i].data_ptr() != o.ctypes.data:
                 o[...] = host_out[i].numpy()
             results.append((o, self._report(info_host, events[i])))
-        del keep
+        del wss
         return results
 
     def solve_async(self, rhs_t, out_t=None, info_t=None):
@@ -468,14 +536,18 @@ class SolverPlan:
         graph = t.cuda.CUDAGraph()
         with t.cuda.graph(graph):
             ws = self._launch(rhs_t, out_t, info_t, stream=t.cuda.current_stream(self._device).cuda_stream)
-        return CapturedSolve(graph, rhs_t, out_t, info_t, ws)
+        return CapturedSolve(graph, rhs_t, out_t, info_t, ws, self)
 
 
 class CapturedSolve:
-    """One solve recorded as a CUDA graph on fixed device buffers (SolverPlan.capture)."""
+    """One solve recorded as a CUDA graph on fixed device buffers (SolverPlan.capture).
 
-    def __init__(self, graph, rhs, out, info, workspace):
+    Holds the plan: the captured kernels read its device tables (twiddles,
+    eigenvalues), which must outlive every replay."""
+
+    def __init__(self, graph, rhs, out, info, workspace, plan):
         self.graph, self.rhs, self.out, self.info, self._ws = graph, rhs, out, info, workspace
+        self._plan = plan
 
     def replay(self):
         self.graph.replay()
