@@ -347,5 +347,63 @@ __device__ __forceinline__ T eig_factor_nz(const Scaling& s, const LineInfo& L, 
 }
 
 // ----------------------------------------------------------------------------
+// Folded DCT-II / DST-II MID step.  The eigenvalue sum of a line is lam_t[k] + C
+// with C = the line's other-axis sum (one add per mode instead of three; the
+// reference's axis order only changes the last bit of lam), and the factor is
+// 1 / lam -- the constant bscale / prod n_p is applied once at the store.
+__device__ __forceinline__ double line_lam_sum(const LineInfo& L) { return L.before + (L.after1 + L.after2); }
+
+template <typename T>
+__device__ __forceinline__ T eig_recip_nz(const double* __restrict__ lam_t, int kt, double C) {
+    const double lam = __ldg(&lam_t[kt]) + C;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
+    double e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    return (T)r;
+}
+// ... and 0 on the null mode (lam == 0)
+template <typename T>
+__device__ __forceinline__ T eig_recip(const double* __restrict__ lam_t, int kt, double C) {
+    const double lam = __ldg(&lam_t[kt]) + C;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
+    double e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-lam, r, 1.0);
+    r = fma(r, e, r);
+    return lam != 0.0 ? (T)r : (T)0;
+}
+
+// One quad {q, n-q, M-q, M+q} (0 < q < M/2) of the DCT-II -> 1/lam -> DCT-III MID
+// on the half-length spectrum pair (zk, zm) = (Z_q, Z_{M-q}), in place.  The
+// untangle, the quarter-wave post-twiddle, the scale, the DCT-III pre-twiddle and
+// the tangle are one real-linear map of (Z_q, Z_{M-q}); with a = w_q, b = w_q t_q
+// (w_q = e^{-i pi q/2n}, t_q = e^{-2 pi i q/n}) and c = 1/sqrt 2:
+//   E = Z_q + conj Z_{M-q},  O = -i (Z_q - conj Z_{M-q}),  P = a E,  Q = b O
+//   P + Q           = 2 w_q V_q           -> (X_q, -X_{n-q})
+//   G = (1 - i) conj(P - Q) = 2 w_{M-q} V_{M-q} / c -> (X_{M-q}, -X_{M+q}) / c
+//   Y = (U.x f_q, U.y f_{n-q}),  Yg = (G.x f_{M-q}, G.y f_{M+q})
+//   H = (1 - i) conj(Yg)   (the inverse's w-twiddle of the mirrored value times 2)
+//   Z'_q = conj(a) (Y + H/2) + i conj(b) (Y - H/2),  Z'_{M-q} = conj(conj(a) (Y + H/2) - i conj(b) (Y - H/2))
+// 40 flops instead of the 64 of the step-by-step form (rsplit / cmul / scale / cmulc / rmerge);
+// identical to it up to rounding.  f* = eigenvalue factors at the PHYSICAL indices.
+template <typename T>
+__device__ __forceinline__ void mid_quad(cx<T>& zk, cx<T>& zm, cx<T> a, cx<T> b, T fq, T fnq, T fmq, T fpq) {
+    const cx<T> E = mkc<T>(zk.x + zm.x, zk.y - zm.y);
+    const cx<T> O = mkc<T>(zk.y + zm.y, zm.x - zk.x);
+    const cx<T> P = cmul<T>(a, E), Q = cmul<T>(b, O);
+    const cx<T> U = cadd<T>(P, Q), D = csub<T>(P, Q);
+    const cx<T> Y = mkc<T>(U.x * fq, U.y * fnq);
+    const cx<T> Yg = mkc<T>((D.x - D.y) * fmq, -(D.x + D.y) * fpq);
+    const cx<T> H = mkc<T>(Yg.x - Yg.y, -(Yg.x + Yg.y));
+    const cx<T> Sp = mkc<T>(fma((T)0.5, H.x, Y.x), fma((T)0.5, H.y, Y.y));
+    const cx<T> Sm = mkc<T>(fma((T)-0.5, H.x, Y.x), fma((T)-0.5, H.y, Y.y));
+    const cx<T> Ep = cmulc<T>(Sp, a), R = cmulc<T>(Sm, b);
+    zk = mkc<T>(Ep.x - R.y, Ep.y + R.x);
+    zm = mkc<T>(Ep.x + R.y, R.x - Ep.y);
+}
 
 }  // namespace fpb

@@ -84,6 +84,17 @@ __device__ __forceinline__ int ikind_of(const FftPass& p) {
     else return p.ikind;
 }
 
+// a MID on DCT-II / DST-II lines runs the folded quad step (fp_common.cuh mid_quad):
+// its factors are 1 / lam and the constant bscale / prod n_p moves to the store
+template <int OP>
+__device__ __forceinline__ bool mid_folded(const FftPass& p) {
+    return opb(OP) == OP_MID && (fkind_of<OP>(p) == FK_DCT2 || fkind_of<OP>(p) == FK_DST2);
+}
+template <int OP>
+__device__ __forceinline__ double mid_store_scale(const FftPass& p) {
+    return mid_folded<OP>(p) ? p.s.bscale * p.s.inv_np : 1.0;
+}
+
 // does this (op, kind) read complex lines?
 template <int OP>
 __device__ __forceinline__ bool complex_input(const FftPass& p) {
@@ -508,7 +519,8 @@ __device__ __forceinline__ bool place_nyquist(const FftPass& p, const LineInfo& 
 
 // store of an inverse-transformed tile (natural-order data in shared memory)
 template <typename T, int LOGM, bool STRIDED, int OP>
-__device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm, int bio_off = 0) {
+__device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineInfo* linfo, cx<T>* sm, int bio_off = 0,
+                                                   double oscale = 1.0) {
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
     const int LS = line_stride<T, LOGM, STRIDED>(p);
@@ -523,7 +535,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
     const LineInfo Lio = linfo[lio];
         if (!Lio.valid) return;
         const int ik = ikind_of<OP>(p);
-        const T om = (T)p.out_mult;
+        const T om = (T)(p.out_mult * oscale);
         const long long ob = Lio.out_off;
         const long long os = g.out_st;
         if (STRIDED && g.blk_lg > 0) {
@@ -931,22 +943,15 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             } else {
                 const bool dst = kind == FK_DST2;
 #define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
-                // U = w * 2V gives X_k = Re U, X_{n-k} = -Im U (the 2 and the 1/2 cancel);
-                // the inverse takes V' = conj(w) (X_k f_k, -X_{n-k} f_{n-k}) = conj(w) (U.x f_k, U.y f_{n-k})
+                const cx<T>* __restrict__ Wb = reinterpret_cast<const cx<T>*>(p.wb);
+                const double* __restrict__ lt = Sc.lam_t;
+                const double C = line_lam_sum(L);
                 auto quad = [&](int q) {
-                    const cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                    const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                    const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                    const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
-                    const cx<T> U2 = cmul<T>(wm, rsplit2<T>(zm, zk, tm));
-                    const cx<T> Y1 = mkc<T>(U1.x * eig_factor_nz<T>(Sc, L, KPHYS(q), cst),
-                                            U1.y * eig_factor_nz<T>(Sc, L, KPHYS(n - q), cst));
-                    const cx<T> Y2 = mkc<T>(U2.x * eig_factor_nz<T>(Sc, L, KPHYS(M - q), cst),
-                                            U2.y * eig_factor_nz<T>(Sc, L, KPHYS(M + q), cst));
-                    const cx<T> Vk = cmulc<T>(Y1, wq);
-                    const cx<T> Vm = cmulc<T>(Y2, wm);
-                    line_f[P(q)] = rmerge<T>(Vk, Vm, tq);
-                    line_f[P(M - q)] = rmerge<T>(Vm, Vk, tm);
+                    cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
+                    mid_quad<T>(zk, zm, Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C), eig_recip_nz<T>(lt, KPHYS(n - q), C),
+                                eig_recip_nz<T>(lt, KPHYS(M - q), C), eig_recip_nz<T>(lt, KPHYS(M + q), C));
+                    line_f[P(q)] = zk;
+                    line_f[P(M - q)] = zm;
                 };
                 if (jt == 0) {
                     const cx<T> z0 = line_f[P(0)];
@@ -954,15 +959,15 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                     T X0 = (T)2 * (z0.x + z0.y);
                     T XM = (T)2 * (z0.x - z0.y) * wM.x;
                     if (cap && !dst) *Sc.dc_out = (double)X0;
-                    X0 *= eig_factor<T>(Sc, L, KPHYS(0));
-                    XM *= eig_factor<T>(Sc, L, KPHYS(M));
+                    X0 *= eig_recip<T>(lt, KPHYS(0), C);
+                    XM *= eig_recip<T>(lt, KPHYS(M), C);
                     const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
                     line_f[P(0)] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
                     const cx<T> zh = line_f[P(HALF)];
                     const cx<T> wh = Ww[HALF], th = Wt[HALF];
                     const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
-                    const T Xa = (T)2 * U.x * eig_factor<T>(Sc, L, KPHYS(HALF));
-                    const T Xb = (T)-2 * U.y * eig_factor<T>(Sc, L, KPHYS(n - HALF));
+                    const T Xa = (T)2 * U.x * eig_recip<T>(lt, KPHYS(HALF), C);
+                    const T Xb = (T)-2 * U.y * eig_recip<T>(lt, KPHYS(n - HALF), C);
                     const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
                     line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
                 } else {
@@ -1041,7 +1046,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
     if constexpr (opb(OP) != OP_FWD) {
         // =============== INVERSE FFT + store (INV and MID)
         fft_tile<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W);
-        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
+        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm, 0, mid_store_scale<OP>(p));
     }
 }
 
@@ -1212,6 +1217,9 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
                 } else {
                     const bool dst = kind == FK_DST2;
 #define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
+                    const cx<T>* __restrict__ Wb = reinterpret_cast<const cx<T>*>(p.wb);
+                    const double* __restrict__ lt = Sc.lam_t;
+                    const double C = line_lam_sum(L);
 #pragma unroll
                     for (int r = 0; r < 8; ++r) {
                         const int q = jt + r * TL;
@@ -1221,29 +1229,20 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
                             T X0 = (T)2 * (z0.x + z0.y);
                             T XM = (T)2 * (z0.x - z0.y) * wM.x;
                             if (cap && !dst) *Sc.dc_out = (double)X0;
-                            X0 *= eig_factor<T>(Sc, L, KPHYS(0));
-                            XM *= eig_factor<T>(Sc, L, KPHYS(M));
+                            X0 *= eig_recip<T>(lt, KPHYS(0), C);
+                            XM *= eig_recip<T>(lt, KPHYS(M), C);
                             const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
                             v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
                             const cx<T> wh = Ww[HALF], th = Wt[HALF];
                             const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
-                            const T Xa = (T)2 * U.x * eig_factor<T>(Sc, L, KPHYS(HALF));
-                            const T Xb = (T)-2 * U.y * eig_factor<T>(Sc, L, KPHYS(n - HALF));
+                            const T Xa = (T)2 * U.x * eig_recip<T>(lt, KPHYS(HALF), C);
+                            const T Xb = (T)-2 * U.y * eig_recip<T>(lt, KPHYS(n - HALF), C);
                             const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
                             half0 = rmerge<T>(Vh, Vh, th);
                         } else {
-                            const cx<T> tq = Wt[q], tm = t_mirror<T>(tq);
-                            const cx<T> wq = Ww[q], wm = w_mirror<T>(wq);
-                            const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
-                            const cx<T> U2 = cmul<T>(wm, rsplit2<T>(pz[r], v[r], tm));
-                            const cx<T> Y1 = mkc<T>(U1.x * eig_factor_nz<T>(Sc, L, KPHYS(q), cst),
-                                                    U1.y * eig_factor_nz<T>(Sc, L, KPHYS(n - q), cst));
-                            const cx<T> Y2 = mkc<T>(U2.x * eig_factor_nz<T>(Sc, L, KPHYS(M - q), cst),
-                                                    U2.y * eig_factor_nz<T>(Sc, L, KPHYS(M + q), cst));
-                            const cx<T> Vk = cmulc<T>(Y1, wq);
-                            const cx<T> Vm = cmulc<T>(Y2, wm);
-                            v[r] = rmerge<T>(Vk, Vm, tq);
-                            pz[r] = rmerge<T>(Vm, Vk, tm);
+                            mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C),
+                                        eig_recip_nz<T>(lt, KPHYS(n - q), C), eig_recip_nz<T>(lt, KPHYS(M - q), C),
+                                        eig_recip_nz<T>(lt, KPHYS(M + q), C));
                         }
                     }
 #undef KPHYS
@@ -1302,7 +1301,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
         // inverse FFT from registers (its first write is preceded by a barrier,
         // so the pre-processing reads above are complete)
         fft_tile_from_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
-        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm);
+        compute_store_tail<T, LOGM, STRIDED, OP>(p, linfo, sm, 0, mid_store_scale<OP>(p));
     }
 }
 

@@ -62,6 +62,7 @@ struct DevTables {
     void* wfft = nullptr;
     void* wt = nullptr;
     void* ww = nullptr;
+    void* wb = nullptr;     // folded DCT-II / DST-II MID twiddle (fp_tables.h mid_table)
     void* mat_f = nullptr;  // dense forward
     void* mat_b = nullptr;  // dense backward
     int fwd_nout = 0, fwd_nin = 0, bwd_nout = 0, bwd_nin = 0;
@@ -664,6 +665,11 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             if ((st = upload(P->allocs, wf, P->f32, &T.wfft)) != FP_OK) { delete P; return st; }
             if ((st = upload(P->allocs, wt, P->f32, &T.wt)) != FP_OK) { delete P; return st; }
             if ((st = upload(P->allocs, ww, P->f32, &T.ww)) != FP_OK) { delete P; return st; }
+            if (cfg->bc[a] != FP_BC_PERIODIC && !regular) {
+                std::vector<long double> wb;
+                mid_table((int)cfg->n[a], Mx[a], wb);
+                if ((st = upload(P->allocs, wb, P->f32, &T.wb)) != FP_OK) { delete P; return st; }
+            }
         } else {
             const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
             const int bk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 101 : FP_IDFT) : bwd[a];
@@ -737,6 +743,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         p.wfft = P->tab[t].wfft;
         p.wt = P->tab[t].wt;
         p.ww = P->tab[t].ww;
+        p.wb = P->tab[t].wb;
         p.out_mult = 1.0;
         Scaling& s = p.s;
         // DST-I spectra sit at k = 1..M-1 of the extended line: eigenvalue k - 1

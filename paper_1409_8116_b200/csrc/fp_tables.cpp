@@ -90,6 +90,11 @@ void fft_tables(int n_real, int M, bool real_kind, std::vector<long double>& wff
     }
 }
 
+void mid_table(int n_real, int M, std::vector<long double>& wb) {
+    wb.assign(2 * (size_t)(M + 1), 0.0L);
+    for (int k = 0; k <= M; ++k) root(5LL * k, 4LL * n_real, &wb[2 * k], &wb[2 * k + 1]);   // e^{-5 i pi k/(2n)}
+}
+
 double axis_dx(const AxisSpec& a) {
     if (a.kind == 1) return a.length / (double)a.n;          // staggered
     if (a.bc == 0) return a.length / (double)a.n;             // periodic

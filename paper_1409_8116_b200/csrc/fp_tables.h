@@ -14,6 +14,9 @@ struct AxisSpec {
 void exact_cis(long long num, long long den, long double* c, long double* s);
 void fft_tables(int n_real, int M, bool real_kind, std::vector<long double>& wfft,
                 std::vector<long double>& wt, std::vector<long double>& ww);
+// w_k t_k = e^{-5 i pi k/(2n)}, k = 0..M: the second twiddle of the folded DCT-II /
+// DST-II MID step (fp_common.cuh mid_quad)
+void mid_table(int n_real, int M, std::vector<long double>& wb);
 double axis_dx(const AxisSpec& a);
 std::vector<double> eigenvalue_table(const AxisSpec& a, int approx);
 // kind: FP_DFT..FP_DCT3, or 100 (real-input DFT half spectrum), 101 (half spectrum -> real)

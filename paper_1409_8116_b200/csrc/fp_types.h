@@ -94,6 +94,7 @@ struct FftPass {
     const void* wfft;           // M roots  e^{-2 pi i k/M}          (Real2)
     const void* wt;             // M+1 roots e^{-2 pi i k/n}  (real kinds)
     const void* ww;             // M+1 roots e^{-i pi k/(2n)} (DCT/DST)
+    const void* wb;             // M+1 roots e^{-5 i pi k/(2n)} = w_k t_k (DCT/DST MID; else nullptr)
     int* nonfinite;             // first pass only
     double out_mult;            // extra output scale (DFT 1/n in TransformPlan)
     Producer prod;              // first pass of a fused projection step (active = 0 otherwise)
