@@ -313,16 +313,42 @@ def mr_fft(z: np.ndarray, inverse: bool = False) -> np.ndarray:
     return w
 
 
-def mr_transform(kind: str, x: np.ndarray) -> np.ndarray:
+def blue_fft(z: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """Unnormalised complex DFT of the last axis by Bluestein's algorithm as the
+    Bluestein engine runs it (csrc/fp_blue.cu): jk = (j^2 + k^2 - (k-j)^2)/2 turns the
+    DFT into Z_k = conj(c_k) sum_j (z_j conj(c_j)) c_{k-j}, c_m = e^{i pi m^2/N}
+    (conjugated for the inverse sign), a linear convolution evaluated as a cyclic one
+    of length L = the power of two >= max(2N - 1, 16); the chirp angle is reduced
+    exactly (m^2 mod 2N) as the plan tables are."""
+    N = z.shape[-1]
+    m = np.arange(N, dtype=np.int64)
+    c = np.exp(1j * np.pi * ((m * m) % (2 * N)) / N)
+    if inverse:
+        c = np.conj(c)
+    L = 16
+    while L < 2 * N - 1:
+        L *= 2
+    h = np.zeros(L, dtype=np.complex128)
+    h[:N] = c
+    h[L - N + 1:] = c[1:][::-1]
+    a = np.zeros(z.shape[:-1] + (L,), dtype=np.complex128)
+    a[..., :N] = z * np.conj(c)
+    conv = np.fft.ifft(np.fft.fft(a) * np.fft.fft(h))
+    return conv[..., :N] * np.conj(c)
+
+
+def mr_transform(kind: str, x: np.ndarray, fft=None) -> np.ndarray:
     """Unnormalised scipy-type transform of the last axis by the mixed-radix recipes
-    (any n: Makhoul for II/III, even/odd extensions for I, full complex FFTs)."""
+    (any n: Makhoul for II/III, even/odd extensions for I, full complex FFTs).
+    `fft` swaps the complex DFT underneath (blue_fft: the Bluestein engine's)."""
+    mr_fft_ = fft or mr_fft
     n = x.shape[-1]
     j = np.arange(n)
     mk = np.where(j % 2 == 0, j // 2, n - 1 - j // 2)           # Makhoul position of x_j
     if kind in ("dct2", "dst2"):
         v = np.empty(x.shape, dtype=np.complex128)
         v[..., mk] = x * ((-1.0) ** j if kind == "dst2" else 1.0)
-        V = mr_fft(v)
+        V = mr_fft_(v)
         y = 2.0 * (np.exp(-1j * np.pi * j / (2 * n)) * V).real
         return y[..., ::-1] if kind == "dst2" else y
     if kind in ("dct3", "dst3"):
@@ -330,20 +356,41 @@ def mr_transform(kind: str, x: np.ndarray) -> np.ndarray:
         Xn = np.concatenate([np.zeros(X.shape[:-1] + (1,)), X[..., :0:-1]], axis=-1)   # X_{n-k}, X_n = 0
         W = np.exp(1j * np.pi * j / (2 * n)) * (X - 1j * Xn)
         W[..., 0] = X[..., 0]
-        y = mr_fft(W, inverse=True)[..., mk].real
+        y = mr_fft_(W, inverse=True)[..., mk].real
         return y * (-1.0) ** j if kind == "dst3" else y
     if kind == "dct1":
         z = np.concatenate([x, x[..., -2:0:-1]], axis=-1)
-        return mr_fft(z.astype(np.complex128))[..., :n].real
+        return mr_fft_(z.astype(np.complex128))[..., :n].real
     if kind == "dst1":
         zero = np.zeros(x.shape[:-1] + (1,))
         z = np.concatenate([zero, x, zero, -x[..., ::-1]], axis=-1)
-        return -mr_fft(z.astype(np.complex128))[..., 1:n + 1].imag
+        return -mr_fft_(z.astype(np.complex128))[..., 1:n + 1].imag
     if kind == "dft":
-        return mr_fft(x.astype(np.complex128)) / n
+        return mr_fft_(x.astype(np.complex128)) / n
     if kind == "idft":
-        return mr_fft(x.astype(np.complex128), inverse=True)
+        return mr_fft_(x.astype(np.complex128), inverse=True)
+    if kind == "rfft":   # real-input DFT, outputs k = 0..n/2 (the plan's kind 100)
+        return mr_fft_(x.astype(np.complex128))[..., : n // 2 + 1]
+    if kind == "irfft":  # half spectrum -> real, unnormalised (kind 101): x has n//2+1 entries
+        raise ValueError("irfft: use blue_irfft(x, n)")
     raise ValueError(kind)
+
+
+def blue_transform(kind: str, x: np.ndarray) -> np.ndarray:
+    """The Bluestein engine's algorithm for every kind (mr_transform's recipes on blue_fft)."""
+    return mr_transform(kind, x, fft=blue_fft)
+
+
+def blue_irfft(X: np.ndarray, n: int, fft=None) -> np.ndarray:
+    """Half spectrum (n//2+1 entries) -> n reals, unnormalised (the plan's kind 101):
+    Hermitian extension, inverse-sign DFT, real part."""
+    fft = fft or blue_fft
+    h = n // 2 + 1
+    k = np.arange(n)
+    src = np.where(k < h, k, n - k)
+    z = X[..., src]
+    z = np.where(k < h, z, np.conj(z))
+    return fft(z.astype(np.complex128), inverse=True).real
 
 
 # -- flow.py: the projection step around the solve (SURVEY.md 8(f)2) ---------------

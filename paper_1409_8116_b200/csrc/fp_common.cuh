@@ -313,20 +313,25 @@ __host__ __device__ __forceinline__ size_t linfo_bytes(int lines) {
     return (sizeof(LineInfo) * (size_t)lines + 15) & ~(size_t)15;
 }
 
+// 1 / x in fp64 from rcp.approx.ftz.f64 (MUFU.RCP64H, 2^-19.9 relative on sm_100a:
+// profiles/r02/rcp_probe.txt) and one cubic refinement r (1 + e + e^2), e = 1 - x r:
+// error <= 1 ulp over 2^28 samples (two Newton steps: 4 DFMA, correctly rounded; this: 3)
+__device__ __forceinline__ double recip_f64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    return fma(r, fma(e, e, e), r);
+}
+
 // eigenvalue factor for transform-axis index kt on line `L`
 template <typename T>
 __device__ __forceinline__ T eig_factor(const Scaling& s, const LineInfo& L, int kt) {
     // absent axes contribute +0.0 (exact), so the adds are unconditional and
     // the sum keeps the reference's axis order ((l0 + l1) + l2)
     const double lam = ((L.before + __ldg(&s.lam_t[kt])) + L.after1) + L.after2;
-    // bscale / lam via rcp.approx + two Newton steps (within 1 ulp of the IEEE
+    // bscale / lam via rcp.approx + a cubic refinement (within 1 ulp of the IEEE
     // quotient of solver.py:158); the null mode (lam == 0) maps to 0
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
-    double e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
+    const double r = recip_f64(lam);
     const double f = lam != 0.0 ? (s.bscale * r) * s.inv_np : 0.0;
     return (T)f;
 }
@@ -337,12 +342,7 @@ __device__ __forceinline__ T eig_factor_nz(const Scaling& s, const LineInfo& L, 
     // absent axes contribute +0.0 (exact), so the adds are unconditional and
     // the sum keeps the reference's axis order ((l0 + l1) + l2)
     const double lam = ((L.before + __ldg(&s.lam_t[kt])) + L.after1) + L.after2;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
-    double e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
+    const double r = recip_f64(lam);
     return (T)(cst * r);
 }
 
@@ -356,24 +356,14 @@ __device__ __forceinline__ double line_lam_sum(const LineInfo& L) { return L.bef
 template <typename T>
 __device__ __forceinline__ T eig_recip_nz(const double* __restrict__ lam_t, int kt, double C) {
     const double lam = __ldg(&lam_t[kt]) + C;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
-    double e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
+    const double r = recip_f64(lam);
     return (T)r;
 }
 // ... and 0 on the null mode (lam == 0)
 template <typename T>
 __device__ __forceinline__ T eig_recip(const double* __restrict__ lam_t, int kt, double C) {
     const double lam = __ldg(&lam_t[kt]) + C;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(lam));
-    double e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-lam, r, 1.0);
-    r = fma(r, e, r);
+    const double r = recip_f64(lam);
     return lam != 0.0 ? (T)r : (T)0;
 }
 

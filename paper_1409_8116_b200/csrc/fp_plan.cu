@@ -36,6 +36,12 @@ size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
 int strided_line_stride(const FftPass& p, bool f32);
 cudaError_t launch_divergence(const Producer& q, void* rhs, bool f32, cudaStream_t st);
 cudaError_t launch_correct(const CorrectPass& c, bool f32, cudaStream_t st);
+cudaError_t launch_blue_gather(const BluePass& p, void* S, long long l0, long long cl, bool f32, cudaStream_t st);
+cudaError_t launch_blue_emit(const BluePass& p, const void* S, long long l0, long long cl, bool f32, cudaStream_t st);
+cudaError_t launch_blue_mul(void* S, const void* bhat, long long cl, int L, bool f32, cudaStream_t st);
+cudaError_t launch_blue_twiddle(void* S, long long cl, int L1, int L2, int inv, bool f32, cudaStream_t st);
+cudaError_t launch_blue_filter(void* S, const void* chirp, int N, int L, int conj, bool f32, cudaStream_t st);
+cudaError_t launch_blue_scale(void* dst, const void* S, int L, double s, bool f32, cudaStream_t st);
 }  // namespace fpb
 
 using namespace fpb;
@@ -55,7 +61,7 @@ static fp_status fail(fp_status st, const std::string& msg) {
 namespace {
 
 enum Buf { B_RHS = 0, B_OUT = 1, B_RS = 2, B_CW = 3, B_X = 4 };  // B_X: caller's exchange buffer (distributed)
-enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2, EN_MR = 3 };
+enum Engine { EN_FFT = 0, EN_DENSE = 1, EN_SCALE = 2, EN_MR = 3, EN_BLUE = 4 };
 enum Layout { LY_REAL = 0, LY_CPLX = 1 };  // state of the data in the buffer
 
 struct DevTables {
@@ -77,6 +83,16 @@ struct DevTables {
     void* mr_root = nullptr;
     void* mr_wq = nullptr;
     void* mr_perm = nullptr;
+    // Bluestein engine (fp_blue.cu): one DFT length N and one convolution length L
+    // (= L1 x L2 four-step when L exceeds the FFT engine's 8192 points) per pair
+    bool blue = false;
+    int bN = 0, bL = 0, bL1 = 1, bL2 = 0;
+    void* b_chirp = nullptr;
+    void* b_wq = nullptr;
+    void* b_bhat_m = nullptr;   // FFT_L of the chirp filter / L (DFT sign -)
+    void* b_bhat_p = nullptr;   // ... of its conjugate (sign +)
+    void* b_w1 = nullptr;       // FFT-engine stage twiddles for M = L1 (four-step only)
+    void* b_w2 = nullptr;       // ... for M = L2 (= L without the four-step)
 };
 
 struct PassT {
@@ -89,6 +105,7 @@ struct PassT {
     DensePass dp;
     MrPass mp;
     ScalePass sp;
+    BluePass bp;
     int a, b;            // other axes (-1 = dummy)
     bool dist_mid;       // MID over the all-to-all receive layout (blocked axis 0)
 };
@@ -126,6 +143,7 @@ struct fp_plan {
     double bscale = 1.0;
     double np_prod = 1.0;
     double null_scale = 1.0;
+    size_t blue_bytes = 0;           // Bluestein scratch (workspace), max over the passes
     std::vector<PassT> passes;
     std::vector<PassT> passes_ovr;   // middle axis split around a dense _inv_lam scale (override solves)
     bool need_cw_ovr = false;
@@ -513,6 +531,177 @@ void fft_tile_shape(FftPass& p, bool f32, bool in_cpx, long long na, long long n
     }
 }
 
+// ---------------------------------------------------------------------------
+// Bluestein engine (fp_blue.cu): plan-time tables and the per-pass launch sequence.
+//
+// FFT_L of `cl` contiguous scratch rows (complex, plan precision) on the FFT
+// engine: one contiguous pass for L <= 8192, else the four-step L1 x L2
+// (strided FFT over j1, twiddle, contiguous FFT over j2; the output sits at
+// k1 L2 + k2 for frequency k1 + L1 k2 -- the filter spectrum uses the same order,
+// and the inverse runs the steps backwards, so no transpose is ever needed).
+cudaError_t blue_cfft(const DevTables& T, void* S, long long cl, bool inv, bool f32, cudaStream_t st) {
+    const int et = f32 ? ET_C64 : ET_C128;
+    auto pass = [&](int M, const void* w, bool strided, long long na, long long nb, long long s_t, long long sa,
+                    long long sb) {
+        FftPass p{};
+        p.op = inv ? OP_INV : OP_FWD;
+        p.fkind = FK_CFFT;
+        p.ikind = IK_ICFFT;
+        p.family = strided ? FAM_STRIDED : FAM_CONTIG;
+        p.n = M;
+        p.M = M;
+        p.logM = ilog2(M);
+        p.ls = p.M + p.M / 16 + 1;
+        if ((p.ls & 1) == 0) p.ls += 1;
+        p.g.na = (int)na;
+        p.g.nb = (int)nb;
+        p.g.in = S;
+        p.g.out = S;
+        p.g.in_type = p.g.out_type = et;
+        p.g.in_st = p.g.out_st = s_t;
+        p.g.in_sa = p.g.out_sa = sa;
+        p.g.in_sb = p.g.out_sb = sb;
+        fft_tile_shape(p, f32, true, na, nb);
+        p.wfft = w;
+        p.out_mult = 1.0;
+        return launch_fft_pass(p, f32, st);
+    };
+    const long long L = T.bL, L1 = T.bL1, L2 = T.bL2;
+    if (L1 == 1) return pass((int)L, T.b_w2, false, cl, 1, 1, L, 0);
+    cudaError_t e;
+    if (!inv) {
+        if ((e = pass((int)L1, T.b_w1, true, cl, L2, L2, L, 1)) != cudaSuccess) return e;
+        if ((e = launch_blue_twiddle(S, cl, (int)L1, (int)L2, 0, f32, st)) != cudaSuccess) return e;
+        return pass((int)L2, T.b_w2, false, cl, L1, 1, L, L2);
+    }
+    if ((e = pass((int)L2, T.b_w2, false, cl, L1, 1, L, L2)) != cudaSuccess) return e;
+    if ((e = launch_blue_twiddle(S, cl, (int)L1, (int)L2, 1, f32, st)) != cudaSuccess) return e;
+    return pass((int)L1, T.b_w1, true, cl, L2, L2, L, 1);
+}
+
+// DFT length of a kind's Bluestein recipe
+long long blue_length(int kind, long long n) {
+    if (kind == FP_DCT1) return 2 * (n - 1);
+    if (kind == FP_DST1) return 2 * (n + 1);
+    return n;
+}
+
+// shortest line that takes the Bluestein engine instead of the dense one
+// (FP_BLUE_MIN overrides; FP_BLUE=0 disables it below the dense engine's cap)
+long long blue_min_length() {
+    static const long long v = [] {
+        const char* e = std::getenv("FP_BLUE");
+        if (e && *e == '0') return (long long)kDenseMax + 1;
+        return (long long)env_int("FP_BLUE_MIN", 128);
+    }();
+    return v;
+}
+
+// tables of a Bluestein axis (pair of kinds with one DFT length); the filter
+// spectra are computed on the device with the same FFT_L the solve uses
+template <typename AllocT>
+fp_status blue_setup(AllocT& allocs, DevTables& T, int fwd_kind, long long n, bool f32) {
+    const long long N = blue_length(fwd_kind, n);
+    long long L = 16;
+    while (L < 2 * N - 1) L *= 2;
+    const long long max_fft = 8192;
+    if (L > max_fft * max_fft) return fail(FP_ERR_UNSUPPORTED, "line too long for the Bluestein engine");
+    T.bN = (int)N;
+    T.bL = (int)L;
+    T.bL1 = 1;
+    T.bL2 = (int)L;
+    if (L > max_fft) {
+        T.bL1 = (int)std::max<long long>(16, L / max_fft);
+        T.bL2 = (int)(L / T.bL1);
+    }
+    fp_status st;
+    std::vector<long double> c(2 * (size_t)N);
+    for (long long m = 0; m < N; ++m) {   // c_m = e^{i pi m^2/N} = e^{2 pi i (m^2 mod 2N)/(2N)}
+        const long long r = (long long)(((unsigned long long)m * (unsigned long long)m) % (unsigned long long)(2 * N));
+        exact_cis(r, 2 * N, &c[2 * m], &c[2 * m + 1]);
+    }
+    if ((st = upload(allocs, c, f32, &T.b_chirp)) != FP_OK) return st;
+    std::vector<long double> r;
+    root_table(4 * n, n + 1, r);   // e^{-i pi k/(2n)}
+    if ((st = upload(allocs, r, f32, &T.b_wq)) != FP_OK) return st;
+    std::vector<long double> wf, wt, ww;
+    fft_tables(T.bL2, T.bL2, false, wf, wt, ww);
+    if ((st = upload(allocs, wf, f32, &T.b_w2)) != FP_OK) return st;
+    if (T.bL1 > 1) {
+        fft_tables(T.bL1, T.bL1, false, wf, wt, ww);
+        if ((st = upload(allocs, wf, f32, &T.b_w1)) != FP_OK) return st;
+    }
+    const size_t cb = (size_t)L * (f32 ? 8 : 16);
+    for (int conj = 0; conj < 2; ++conj) {
+        void* bh = nullptr;
+        CUDA_TRY(cudaMalloc(&bh, cb));
+        allocs.push_back(bh);
+        (conj ? T.b_bhat_p : T.b_bhat_m) = bh;
+    }
+    void* S = nullptr;
+    CUDA_TRY(cudaMalloc(&S, cb));
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) { cudaFree(S); return fail(FP_ERR_CUDA, "stream"); }
+    cudaError_t e = cudaSuccess;
+    for (int conj = 0; conj < 2 && e == cudaSuccess; ++conj) {
+        e = launch_blue_filter(S, T.b_chirp, (int)N, (int)L, conj, f32, s);
+        if (e == cudaSuccess) e = blue_cfft(T, S, 1, false, f32, s);
+        if (e == cudaSuccess) e = launch_blue_scale(conj ? T.b_bhat_p : T.b_bhat_m, S, (int)L, 1.0 / (double)L, f32, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaFree(S);
+    if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("Bluestein filter spectrum: ") + cudaGetErrorString(e));
+    T.blue = true;
+    return FP_OK;
+}
+
+// the pass descriptor of one Bluestein transform (geometry filled at solve time)
+BluePass blue_pass(const DevTables& T, int kind, long long n, long long na, long long nb) {
+    BluePass p{};
+    p.kind = kind;
+    p.n = (int)n;
+    p.n_out = kind == MR_RFFT ? (int)(n / 2 + 1) : (int)n;
+    p.N = T.bN;
+    p.L = T.bL;
+    p.inv = (kind == FP_IDFT || kind == MR_IRFFT || kind == FP_DCT3 || kind == FP_DST3) ? 1 : 0;
+    p.g.na = (int)na;
+    p.g.nb = (int)nb;
+    p.chirp = T.b_chirp;
+    p.wq = T.b_wq;
+    p.out_mult = 1.0;
+    return p;
+}
+
+// scratch bytes of one Bluestein pass: whole chunks of rows, at most ~256 MB
+size_t blue_scratch_bytes(const DevTables& T, long long lines, bool f32) {
+    const size_t row = (size_t)T.bL * (f32 ? 8 : 16);
+    const size_t cap = (size_t)env_int("FP_BLUE_SCRATCH_MB", 256) << 20;
+    long long cl = (long long)std::max<size_t>(1, cap / row);
+    if (cl > lines) cl = lines;
+    return row * (size_t)std::max<long long>(cl, 1);
+}
+
+// one Bluestein pass over every line, in chunks that fit `scratch`
+cudaError_t run_blue(const DevTables& T, const BluePass& p, void* scratch, size_t scratch_bytes, bool f32,
+                     cudaStream_t st) {
+    const long long nl = (long long)p.g.na * p.g.nb;
+    const size_t row = (size_t)p.L * (f32 ? 8 : 16);
+    const long long cmax = (long long)(scratch_bytes / row);
+    if (cmax < 1) return cudaErrorInvalidValue;
+    const void* bhat = p.inv ? T.b_bhat_p : T.b_bhat_m;
+    cudaError_t e = cudaSuccess;
+    for (long long l0 = 0; l0 < nl && e == cudaSuccess; l0 += cmax) {
+        const long long cl = std::min(cmax, nl - l0);
+        if ((e = launch_blue_gather(p, scratch, l0, cl, f32, st)) != cudaSuccess) break;
+        if ((e = blue_cfft(T, scratch, cl, false, f32, st)) != cudaSuccess) break;
+        if ((e = launch_blue_mul(scratch, bhat, cl, p.L, f32, st)) != cudaSuccess) break;
+        if ((e = blue_cfft(T, scratch, cl, true, f32, st)) != cudaSuccess) break;
+        e = launch_blue_emit(p, scratch, l0, cl, f32, st);
+    }
+    return e;
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------------------
@@ -677,10 +866,12 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             T.bwd_kind = bk;
             if ((st = mr_setup(P->allocs, T, fk, cfg->n[a], P->f32)) != FP_OK) { delete P; return st; }
             if (T.mr) continue;
-            if (cfg->n[a] > kDenseMax) {
-                delete P;
-                return fail(FP_ERR_UNSUPPORTED, "axis length " + std::to_string(cfg->n[a]) +
-                                                    " has a prime factor above 61 and needs the dense engine, limited to n <= 8192 in this build");
+            if (cfg->n[a] > kDenseMax || cfg->n[a] >= blue_min_length()) {
+                // a prime factor above 61 (or a line too long for one CTA): Bluestein
+                T.fwd_kind = fk;
+                T.bwd_kind = bk;
+                if ((st = blue_setup(P->allocs, T, fk, cfg->n[a], P->f32)) != FP_OK) { delete P; return st; }
+                continue;
             }
             std::vector<double> m;
             int no, ni;
@@ -767,6 +958,15 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         ps.out_layout = out_cpx ? LY_CPLX : LY_REAL;
         other_axes(t, &ps.a, &ps.b);
         const DevTables& T = P->tab[t];
+        if (T.blue) {
+            ps.engine = EN_BLUE;
+            const long long* ext = complex_state ? P->cext : P->n;
+            const long long na = ps.a >= 0 ? ext[ps.a] : 1;
+            const long long nb = ps.b >= 0 ? ext[ps.b] : 1;
+            ps.bp = blue_pass(T, forward ? T.fwd_kind : T.bwd_kind, cfg->n[t], na, nb);
+            P->blue_bytes = std::max(P->blue_bytes, blue_scratch_bytes(T, na * nb, P->f32));
+            return ps;
+        }
         if (T.mr) {
             ps.engine = EN_MR;
             const long long* ext = complex_state ? P->cext : P->n;
@@ -977,6 +1177,7 @@ FP_API fp_status fp_plan_workspace_bytes_ex(const fp_plan* P, int out_dense, int
     size_t b = cw_bytes(P, inv_lam_override != 0);
     // with a strided `out` the real scratch (also the dtype-cast target) lives here
     if (!out_dense) b += rs_bytes(P);
+    b += align_up(P->blue_bytes);
     b += mean_bytes(P);
     *bytes = b;
     return FP_OK;
@@ -1066,6 +1267,8 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
         }
     }
     double* mean_ws = P->mean_fix ? (double*)((char*)workspace + need - mean_bytes(P)) : nullptr;
+    const size_t blue_b = align_up(P->blue_bytes);
+    void* blue_ws = blue_b ? (void*)((char*)workspace + need - mean_bytes(P) - blue_b) : nullptr;
     const int plan_type = P->f32 ? ET_F32 : ET_F64;
     const int plan_ctype = P->f32 ? ET_C64 : ET_C128;
 
@@ -1159,6 +1362,12 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
             p.g = g;
             p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
             e = launch_dense_pass(p, P->f32, st);
+        } else if (T.engine == EN_BLUE) {
+            BluePass p = T.bp;
+            g.na = p.g.na; g.nb = p.g.nb;
+            p.g = g;
+            p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
+            e = run_blue(P->tab[T.t], p, blue_ws, blue_b, P->f32, st);
         } else {
             ScalePass p = T.sp;
             const bool cpx = T.in_layout == LY_CPLX;
@@ -1453,7 +1662,12 @@ FP_API fp_status fp_transform_create(int kind, int64_t n, int precision, int dev
     } else {
         if ((st = mr_setup(T->allocs, T->tab, kind, n, T->f32)) != FP_OK) { delete T; return st; }
         if (T->tab.mr) { *out = T; return FP_OK; }
-        if (n > kDenseMax) { delete T; return fail(FP_ERR_UNSUPPORTED, "transform length has a prime factor above 61 and needs the dense engine (n <= 8192)"); }
+        if (n > kDenseMax || n >= blue_min_length()) {   // Bluestein
+            T->tab.fwd_kind = kind;
+            if ((st = blue_setup(T->allocs, T->tab, kind, n, T->f32)) != FP_OK) { delete T; return st; }
+            *out = T;
+            return FP_OK;
+        }
         std::vector<double> m;
         int no, ni;
         bool cpx;
@@ -1524,6 +1738,20 @@ FP_API fp_status fp_transform_execute(const fp_transform* T, int ndim, const int
         p.nonfinite = nullptr;
         p.s = Scaling{};
         e = launch_fft_pass(p, T->f32, (cudaStream_t)stream);
+    } else if (T->tab.blue) {
+        // scratch from the stream-ordered allocator (the transform API has no workspace)
+        BluePass p = blue_pass(T->tab, T->kind, T->n, g.na, g.nb);
+        p.g = g;
+        p.out_mult = om;
+        const size_t sb = blue_scratch_bytes(T->tab, (long long)g.na * g.nb, T->f32);
+        void* S = nullptr;
+        cudaStream_t s = (cudaStream_t)stream;
+        e = cudaMallocAsync(&S, sb, s);
+        if (e == cudaSuccess) {
+            e = run_blue(T->tab, p, S, sb, T->f32, s);
+            const cudaError_t e2 = cudaFreeAsync(S, s);
+            if (e == cudaSuccess) e = e2;
+        }
     } else if (T->tab.mr) {
         MrPass p = mr_pass(T->tab, T->kind, T->n, g.na, g.nb, T->f32, g.in_st != 1);
         p.g = g;

@@ -149,6 +149,25 @@ struct MrPass {
     const void* wt;             // half: n/2 + 1 roots e^{-2 pi i k/n}
 };
 
+// Bluestein (chirp-z) engine (fp_blue.cu): any line length, any kind -- the axes
+// neither the FFT nor the mixed-radix engine takes (a prime factor above 61, or
+// lines longer than a CTA's shared memory).  One pass = per chunk of lines:
+// gather (recipe x pre-chirp, zero pad to L) -> FFT_L -> x filter spectrum ->
+// inverse FFT_L -> emit (post-chirp x output recipe); FFT_L on the FFT engine.
+struct BluePass {
+    int kind;                   // public FP_* kind, or MR_RFFT / MR_IRFFT
+    int n;                      // line length
+    int n_out;                  // outputs per line
+    int N;                      // DFT length of the recipe: n, 2(n-1) (DCT-I), 2(n+1) (DST-I)
+    int L;                      // cyclic convolution length (power of two >= 2N - 1, >= 16)
+    int inv;                    // DFT sign of the recipe: 1 = e^{+2 pi i jk/N}
+    Geometry g;
+    const void* chirp;          // N entries c_m = e^{i pi m^2/N} (plan precision, complex)
+    const void* wq;             // n+1 entries e^{-i pi k/(2n)} (II / III kinds; else nullptr)
+    int* nonfinite;
+    double out_mult;
+};
+
 // the projection corrector (flow.py:125-139, 292-295):
 //   u -= scale * (phi[i][j] - phi[i-1][j]) / dx,  w -= scale * (phi[i][j] - phi[i][j-1]) / dz
 // (wall faces keep w), optionally p += phi; dense C-order (nx, nz) / (nx, nz[+1]) arrays

@@ -11,11 +11,15 @@ Definitions (unnormalized forward sums; DFT carries 1/n on the forward leg),
     DCT-III  f_0 + 2 sum_{j>0} f_j cos(pi j (k+1/2)/n)
     DFT      (1/n) sum f_j e^{-2 pi i k j/n};  IDFT  sum f^_k e^{+2 pi i k j/n}
 
-Execution is on the GPU through the native library: power-of-two lengths on
-the FFT line engine (half-length complex FFT + pre/post twiddles), every other
-length/kind on the dense direct-summation engine with correctly rounded
-coefficients.  ``naive_transform`` is the literal O(n^2) host evaluation kept
-as part of the public API (transforms.py:188-229).
+Execution is on the GPU through the native library, one engine per (kind, n):
+power-of-two lengths on the FFT line engine (half-length complex FFT + pre/post
+twiddles); lengths whose FFT length factors into primes <= 61 on the mixed-radix
+engine (csrc/fp_mr.cu); any other length on the Bluestein (chirp-z) engine
+(csrc/fp_blue.cu: a zero-padded power-of-two convolution on the FFT engine,
+four-step beyond 8192 points), except short lines (n < 128), which stay on the
+dense direct-summation engine with correctly rounded coefficients.  Every n is
+supported, as in the reference (scipy.fft).  ``naive_transform`` is the literal
+O(n^2) host evaluation kept as part of the public API (transforms.py:188-229).
 """
 
 from __future__ import annotations

@@ -74,10 +74,10 @@ def test_fp64_type1_beyond_dense_limit(kind, n, torch_cuda, rng):
     _check_transform(kind, n, 0, [n, 3], torch_cuda, rng)
 
 
-def test_large_prime_length_is_unsupported(torch_cuda):
-    # 8209 is prime: no mixed-radix plan, beyond the dense engine -> NotImplementedError, no fallback
-    with pytest.raises(NotImplementedError):
-        fp.TransformPlan(fp.TransformKind.DCT2, 8209, axis=0).execute(torch_cuda.zeros((8209, 2), dtype=torch_cuda.float64, device="cuda"))
+def test_large_prime_length_beyond_dense_limit(torch_cuda, rng):
+    # 8209 is prime: no mixed-radix plan, beyond the dense engine -- the Bluestein engine
+    # (fp_blue.cu) takes it (it used to raise NotImplementedError)
+    _check_transform(fp.TransformKind.DCT2, 8209, 0, [8209, 2], torch_cuda, rng)
 
 
 def _solve_case(axes, approx, precision, torch_cuda, rng, device=False):

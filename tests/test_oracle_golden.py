@@ -107,6 +107,39 @@ def test_mixed_radix_recipes_match_scipy(n, rng):
         np.testing.assert_allclose(orc.mr_transform(kind, xx), want, atol=1e-13 * n * np.abs(want).max())
 
 
+@pytest.mark.parametrize("n", [2, 3, 16, 67, 97, 131, 250, 1009])
+def test_bluestein_recipes_match_scipy(n, rng):
+    # the Bluestein engine's algorithm (fp_blue.cu: chirp, zero-padded cyclic convolution of
+    # power-of-two length, the same recipes as the mixed-radix engine) against scipy.fft at
+    # lengths with large prime factors, plus the real FFT and its inverse (plan kinds 100/101)
+    x = rng.standard_normal((3, n))
+    c = x + 1j * rng.standard_normal((3, n))
+    for kind in ("dct1", "dct2", "dct3", "dst1", "dst2", "dst3", "dft", "idft"):
+        if kind == "dct1" and n < 2:
+            continue
+        xx = c if kind in ("dft", "idft") else x
+        want = orc.forward_1d(kind, xx)
+        np.testing.assert_allclose(orc.blue_transform(kind, xx), want, atol=1e-13 * n * np.abs(want).max())
+    want = np.fft.rfft(x)
+    np.testing.assert_allclose(orc.blue_transform("rfft", x), want, atol=1e-13 * n * np.abs(want).max())
+    X = np.fft.rfft(x)
+    np.testing.assert_allclose(orc.blue_irfft(X, n), n * np.fft.irfft(X, n), atol=1e-12 * n * np.abs(x).max())
+
+
+def test_bluestein_matches_golden_transforms(golden):
+    meta, arrays = golden
+    seen = 0
+    for e in meta["transforms"]:
+        n = e["n"]
+        if n < 2:
+            continue
+        x = arrays[f"{e['id']}/x"]
+        y = arrays[f"{e['id']}/y"]
+        assert np.abs(orc.blue_transform(e["kind"], x) - y).max() <= 1e-12 * n * max(np.abs(x).max(), 1.0), e["id"]
+        seen += 1
+    assert seen > 50
+
+
 def test_mixed_radix_matches_golden_transforms(golden):
     meta, arrays = golden
     seen = 0
