@@ -115,6 +115,7 @@ typedef struct fp_plan_info {
     int num_passes;         /* kernel launches per solve     */
     int middle_axis;        /* axis of the fused forward/scale/inverse pass */
     int fft_axes_mask;      /* axes on the FFT engine (others: dense engine) */
+    int exact_mean;         /* DCT-I plan: explicit arithmetic-mean removal after the backward pass */
 } fp_plan_info;
 
 /* Device-side per-solve record written by the kernels. */
@@ -220,16 +221,20 @@ FP_API fp_status fp_project_correct(const fp_plan* plan, const void* phi, const 
                                     double scale, void* stream);
 
 /* ---- slab decomposition over P ranks (axis 0 split; one all-to-all each way) ----
- * Rank r owns planes [r*local_n0, (r+1)*local_n0) of axis 0 (local arrays are
- * (local_n0, n1, n2) with any strides).  A solve is three phases with two
+ * Any P <= n0: rank r owns planes [offset0, offset0 + local_n0) of axis 0, a balanced
+ * split (the first n0 % P ranks hold one plane more; local arrays are (local_n0, n1,
+ * n2) with any strides).  Axis 0 must be on the FFT engine (power-of-two length); a
+ * wall axis 0 may follow periodic local axes (its MID then runs on the real view of
+ * the complex state); DCT-I axes are single-GPU only.  A solve is three phases with two
  * all-to-alls of exchange_bytes between them, done by the caller (NCCL):
  *   fp_solve_phase(plan, 0, rhs_local, ..., xbuf=send)    local transforms, packed send
  *   all_to_all(send -> recv)                              equal blocks of exchange_bytes/P
  *   fp_solve_phase(plan, 1, ..., xbuf=recv)               MID along the global axis 0
  *   all_to_all(recv -> send)
  *   fp_solve_phase(plan, 2, ..., out_local, xbuf=send)    local inverse transforms
- * The exchange buffer holds (local_n0, exch_n1, exch_n2) elements with axis 1
- * outermost (exch_n1 = n1 or its half spectrum, padded to a multiple of P).
+ * The exchange buffer holds (pitch_n0, exch_n1, exch_n2) elements with axis 1
+ * outermost (exch_n1 = n1 or its half spectrum, padded to a multiple of P; planes
+ * >= local_n0 of a block are padding).
  * Only rank 0's dev_info receives the null coefficient. */
 typedef struct fp_dist_info {
     int nranks, rank;
@@ -243,10 +248,19 @@ typedef struct fp_dist_info {
     int r_axis;             /* periodic axis transformed as a real FFT (-1: none) */
     int elem_bytes;
     size_t exchange_bytes;  /* size of the send and of the receive buffer */
+    int64_t pitch_n0;       /* planes per rank block in the exchange buffers (max local_n0) */
 } fp_dist_info;
 
 FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_dist_info* info); /* no device */
 FP_API fp_status fp_plan_create_dist(const fp_config* cfg, int device, int nranks, int rank, fp_plan** plan);
+/* DCT-I plans (fp_plan_info.exact_mean) over ranks: after phase 2 the caller removes the
+ * GLOBAL arithmetic mean (solver.py:224-225): fp_dist_mean_partial writes this rank's sum of
+ * out_local into *dev_sum (device double; workspace from fp_plan_workspace_bytes), the
+ * caller all-reduces it (SUM), fp_dist_mean_subtract subtracts dev_total / (n0 n1 n2). */
+FP_API fp_status fp_dist_mean_partial(const fp_plan* plan, void* out_local, const int64_t* out_strides,
+                                      void* workspace, size_t workspace_bytes, void* stream, double* dev_sum);
+FP_API fp_status fp_dist_mean_subtract(const fp_plan* plan, void* out_local, const int64_t* out_strides,
+                                       const double* dev_total, void* stream);
 FP_API fp_status fp_solve_phase(const fp_plan* plan, int phase,
                                 const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
                                 void* out, const int64_t* out_strides, void* xbuf,

@@ -52,6 +52,7 @@ class FpPlanInfo(Structure):
         ("num_passes", c_int),
         ("middle_axis", c_int),
         ("fft_axes_mask", c_int),
+        ("exact_mean", c_int),
     ]
 
 
@@ -66,6 +67,7 @@ class FpDistInfo(Structure):
         ("exch_n1", c_int64), ("true_n1", c_int64), ("exch_n2", c_int64), ("block_n1", c_int64),
         ("exch_complex", c_int), ("r_axis", c_int), ("elem_bytes", c_int),
         ("exchange_bytes", c_size_t),
+        ("pitch_n0", c_int64),
     ]
 
 
@@ -126,6 +128,10 @@ SIGNATURES = {
         [c_void_p, c_int, c_void_p, c_int, POINTER(c_int64), c_void_p, POINTER(c_int64), c_void_p, c_void_p,
          c_size_t, c_void_p, c_void_p],
     ),
+    "fp_dist_mean_partial": (
+        c_int, [c_void_p, c_void_p, POINTER(c_int64), c_void_p, c_size_t, c_void_p, c_void_p],
+    ),
+    "fp_dist_mean_subtract": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_void_p, c_void_p]),
     "fp_event_create": (c_int, [POINTER(c_void_p)]),
     "fp_event_create_on": (c_int, [c_int, POINTER(c_void_p)]),
     "fp_event_destroy": (c_int, [c_void_p]),

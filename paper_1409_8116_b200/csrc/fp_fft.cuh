@@ -123,12 +123,14 @@ __device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo
         valid = ib < g.nb;
         if (!valid) ib = 0;
     }
-    const int iag = ia + g.a_off, ibg = ib + g.b_off;   // global line indices
+    const int part = g.pair_b ? (ib & 1) : 0;           // real view: 0 = real, 1 = imaginary part
+    const int ibc = g.pair_b ? (ib >> 1) : ib;
+    const int iag = ia + g.a_off, ibg = ibc + g.b_off;   // global line indices
     if ((g.a_lim > 0 && iag >= g.a_lim) || (g.b_lim > 0 && ibg >= g.b_lim)) valid = false;
     L.valid = valid;
-    L.in_off = (long long)ia * g.in_sa + (long long)ib * g.in_sb;
-    L.out_off = (long long)ia * g.out_sa + (long long)ib * g.out_sb;
-    L.null_line = (iag == 0 && ibg == 0);
+    L.in_off = (long long)ia * g.in_sa + (long long)ibc * g.in_sb + part;
+    L.out_off = (long long)ia * g.out_sa + (long long)ibc * g.out_sb + part;
+    L.null_line = (iag == 0 && ibg == 0 && part == 0);
     double before = 0.0, a1 = 0.0, a2 = 0.0;
     int nafter = 0;
     if (opb(OP) == OP_MID) {
@@ -174,24 +176,27 @@ __device__ __forceinline__ void load_real(T* v, const T* base, long long st, boo
 }
 // blocked transform axis (distributed exchange layout): row j at
 // (j >> lg) * hi + (j & (2^lg - 1)) * st
+// (or, with g.row_tab, at row_tab[j]: uneven slabs / any rank count)
+__device__ __forceinline__ bool blocked(const Geometry& g) { return g.blk_lg > 0 || g.row_tab != nullptr; }
+__device__ __forceinline__ long long blk_row(const Geometry& g, int j, long long st, long long hi) {
+    if (g.row_tab) return __ldg(&g.row_tab[j]);
+    const int lg = g.blk_lg, msk = (1 << lg) - 1;
+    return (long long)(j >> lg) * hi + (long long)(j & msk) * st;
+}
 template <typename T, int CNT, int STEP>
-__device__ __forceinline__ void load_real_blk(T* v, const T* line, int j0, long long st, long long hi, int lg,
-                                              bool valid) {
-    const int msk = (1 << lg) - 1;
+__device__ __forceinline__ void load_real_blk(T* v, const T* line, int j0, const Geometry& g, bool valid) {
 #pragma unroll
     for (int it = 0; it < CNT; ++it) {
         const int j = j0 + it * STEP;
-        v[it] = valid ? __ldg(line + (long long)(j >> lg) * hi + (long long)(j & msk) * st) : (T)0;
+        v[it] = valid ? __ldg(line + blk_row(g, j, g.in_st, g.in_st_hi)) : (T)0;
     }
 }
 template <typename T, int CNT, int STEP>
-__device__ __forceinline__ void load_cx_blk(cx<T>* v, const cx<T>* line, int j0, long long st, long long hi, int lg,
-                                            bool valid) {
-    const int msk = (1 << lg) - 1;
+__device__ __forceinline__ void load_cx_blk(cx<T>* v, const cx<T>* line, int j0, const Geometry& g, bool valid) {
 #pragma unroll
     for (int it = 0; it < CNT; ++it) {
         const int j = j0 + it * STEP;
-        v[it] = valid ? __ldg(line + (long long)(j >> lg) * hi + (long long)(j & msk) * st) : mkc<T>(0, 0);
+        v[it] = valid ? __ldg(line + blk_row(g, j, g.in_st, g.in_st_hi)) : mkc<T>(0, 0);
     }
 }
 
@@ -355,10 +360,12 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
                     z[2 * it + 1] = Lio.valid ? __ldg(rline + (long long)i1 * st) : (T)0;
                 }
             } else {
+                const bool blk = blocked(p.g);   // distributed MID: the receive layout
 #pragma unroll
                 for (int it = 0; it < 32; ++it) {
                     const int i0 = r1_src<M>(d1, 32 * bio + it, &sg[it]);
-                    z[it] = Lio.valid ? __ldg(rline + (long long)i0 * st) : (T)0;
+                    const long long o = blk ? blk_row(p.g, i0, st, p.g.in_st_hi) : (long long)i0 * st;
+                    z[it] = Lio.valid ? __ldg(rline + o) : (T)0;
                 }
             }
             if (chk) {
@@ -427,7 +434,7 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
             }
         } else {
             T xr[32];
-            if (p.g.blk_lg > 0) load_real_blk<T, 32, 1>(xr, rline, 32 * bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+            if (blocked(p.g)) load_real_blk<T, 32, 1>(xr, rline, 32 * bio, p.g, Lio.valid);
             else load_real<T, 32, 1>(xr, rline + (long long)(32 * bio) * st, st, Lio.valid);
             const RowBlk rb(bio, n);
             if (chk) {
@@ -445,7 +452,7 @@ __device__ __forceinline__ bool place_tile(const FftPass& p, const LineInfo& Lio
         }
     } else if (complex_input<OP>(p)) {
         if constexpr (STRIDED) {
-            if (p.g.blk_lg > 0) load_cx_blk<T, 16, 1>(v, cline, 16 * bio, st, p.g.in_st_hi, p.g.blk_lg, Lio.valid);
+            if (blocked(p.g)) load_cx_blk<T, 16, 1>(v, cline, 16 * bio, p.g, Lio.valid);
             else load_cx<T, 16, 1>(v, cline + (long long)(16 * bio) * st, st, Lio.valid, false);
             if (chk) {
 #pragma unroll
@@ -538,16 +545,25 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
         const T om = (T)(p.out_mult * oscale);
         const long long ob = Lio.out_off;
         const long long os = g.out_st;
-        if (STRIDED && g.blk_lg > 0) {
+        if (STRIDED && blocked(g)) {
             // distributed exchange layout: blocked transform axis
-            const int lg = g.blk_lg, msk = (1 << lg) - 1;
             const long long hi = g.out_st_hi;
             if (ik == IK_ICFFT) {
                 cx<T>* pb = reinterpret_cast<cx<T>*>(g.out) + ob;
 #pragma unroll
                 for (int it = 0; it < 16; ++it) {
                     const int k = bio + it * TL;
-                    pb[(long long)(k >> lg) * hi + (long long)(k & msk) * os] = cscale<T>(line_io[P(k)], om);
+                    pb[blk_row(g, k, os, hi)] = cscale<T>(line_io[P(k)], om);
+                }
+            } else if (ik >= IK_DCT1) {
+                // DCT-I keeps z_0..z_M, DST-I z_1..z_{M-1} (shifted down by one)
+                const bool d1 = ik == IK_DCT1;
+                T* pb = reinterpret_cast<T*>(g.out) + ob;
+#pragma unroll
+                for (int it = 0; it < 32; ++it) {
+                    const int j = bio + it * TL;
+                    const T x = zr_io[2 * P(j >> 1) + (j & 1)];
+                    if (d1 ? (j <= M) : (j >= 1 && j < M)) pb[blk_row(g, d1 ? j : j - 1, os, hi)] = x * om;
                 }
             } else {
                 const bool dct = ik == IK_DCT3 || ik == IK_DST3;
@@ -559,7 +575,7 @@ __device__ __forceinline__ void compute_store_tail(const FftPass& p, const LineI
                     const int pv = dct ? ((j & 1) ? (n - 1 - (j >> 1)) : (j >> 1)) : j;
                     T x = zr_io[2 * P(pv >> 1) + (pv & 1)];
                     if (dst && (j & 1)) x = -x;
-                    pb[(long long)(j >> lg) * hi + (long long)(j & msk) * os] = x * om;
+                    pb[blk_row(g, j, os, hi)] = x * om;
                 }
             }
             return;
@@ -1478,11 +1494,8 @@ __device__ __forceinline__ void issue_tile_async(const FftPass& p, const LineInf
     cx<T>* line = sm + lio * LS;
     T* zr = reinterpret_cast<T*>(line);
     const long long st = g.in_st;
-    const bool blk = g.blk_lg > 0;
-    const int lg = g.blk_lg, msk = (1 << (lg > 0 ? lg : 0)) - 1;
-    auto row_off = [&](int j) -> long long {
-        return blk ? (long long)(j >> lg) * g.in_st_hi + (long long)(j & msk) * st : (long long)j * st;
-    };
+    const bool blk = blocked(g);
+    auto row_off = [&](int j) -> long long { return blk ? blk_row(g, j, st, g.in_st_hi) : (long long)j * st; };
     const bool cin = complex_input<OP>(p);
     if (cin) {
         const cx<T>* src = reinterpret_cast<const cx<T>*>(g.in) + L.in_off;

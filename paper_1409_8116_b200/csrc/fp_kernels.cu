@@ -369,14 +369,17 @@ __global__ void __launch_bounds__(256) mean_final_kernel(const MeanPass p, int n
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) acc += p.partials[i];
     const double s = block_sum<T>(acc, red);
     const double total = (double)p.ext[0] * p.ext[1] * p.ext[2];
-    if (threadIdx.x == 0) p.partials[nparts] = s / total;
+    if (threadIdx.x == 0) {
+        if (p.sum_out) *p.sum_out = s;          // distributed: local sum only
+        else p.partials[nparts] = s / total;
+    }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(256) mean_sub_kernel(const MeanPass p, int nparts) {
     const long long total = (long long)p.ext[0] * p.ext[1] * p.ext[2];
     T* d = reinterpret_cast<T*>(p.data);
-    const T m = (T)p.partials[nparts];
+    const T m = p.mean_in ? (T)(*p.mean_in * p.inv_total) : (T)p.partials[nparts];
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
         const long long off = mean_offset<T>(p, i);
         d[off] = d[off] - m;
@@ -616,14 +619,15 @@ cudaError_t launch_mean_pass(const MeanPass& p, bool f32, cudaStream_t st) {
     if (blocks > kMeanParts) blocks = kMeanParts;
     if (blocks < 1) blocks = 1;
     const int nb = (int)blocks;
+    const bool reduce = p.mean_in == nullptr, sub = p.sum_out == nullptr;
     if (f32) {
-        mean_partial_kernel<float><<<nb, 256, 0, st>>>(p);
-        mean_final_kernel<float><<<1, 256, 0, st>>>(p, nb);
-        mean_sub_kernel<float><<<nb, 256, 0, st>>>(p, nb);
+        if (reduce) mean_partial_kernel<float><<<nb, 256, 0, st>>>(p);
+        if (reduce) mean_final_kernel<float><<<1, 256, 0, st>>>(p, nb);
+        if (sub) mean_sub_kernel<float><<<nb, 256, 0, st>>>(p, nb);
     } else {
-        mean_partial_kernel<double><<<nb, 256, 0, st>>>(p);
-        mean_final_kernel<double><<<1, 256, 0, st>>>(p, nb);
-        mean_sub_kernel<double><<<nb, 256, 0, st>>>(p, nb);
+        if (reduce) mean_partial_kernel<double><<<nb, 256, 0, st>>>(p);
+        if (reduce) mean_final_kernel<double><<<1, 256, 0, st>>>(p, nb);
+        if (sub) mean_sub_kernel<double><<<nb, 256, 0, st>>>(p, nb);
     }
     return cudaGetLastError();
 }

@@ -135,7 +135,10 @@ struct fp_plan {
     bool mean_fix = false;           // exact arithmetic-mean removal (DCT-I axes)
     // slab decomposition along axis 0
     int nranks = 1, rank = 0;
-    long long a0 = 0;                // planes per rank
+    long long a0 = 0;                // planes of this rank
+    long long A = 0;                 // plane pitch of the exchange blocks (max planes per rank)
+    bool wall0_cpx = false;          // wall axis 0 after a complex local state: real-view MID
+    const long long* row_tab = nullptr;   // uneven slabs / non-power-of-two pitch: MID row table
     long long E1 = 0, B = 0;         // exchanged extent of axis 1 (padded to P) and per-peer block
     long long e1 = 0, e2 = 1;        // true extents of axes 1, 2 in the exchanged state
     bool x_cpx = false;              // exchanged state complex?
@@ -707,34 +710,46 @@ cudaError_t run_blue(const DevTables& T, const BluePass& p, void* scratch, size_
 // ----------------------------------------------------------------------------
 // Slab decomposition layout (device-free; shared by the planner and fp_dist_layout).
 struct DistLayout {
-    long long a0, e1, e2, E1, B;
+    long long a0, off0, A;           // this rank's planes of axis 0, its first plane, the exchange pitch
+    long long q, r;                  // balanced split: ranks < r own q + 1 planes, the others q
+    long long e1, e2, E1, B;
     int r_axis;
     bool cpx;
+    bool wall0_cpx;                  // wall axis 0 on a complex state: the MID runs on its real view
 };
 
-static fp_status dist_layout(const fp_config* cfg, int nranks, DistLayout* L) {
+// first global plane of rank `k` under the balanced split
+static long long dist_off(const DistLayout& L, long long k) { return k * L.q + std::min(k, L.r); }
+
+static fp_status dist_layout(const fp_config* cfg, int nranks, int rank, DistLayout* L) {
     const int d = cfg->ndim;
     if (nranks < 1) return fail(FP_ERR_VALUE, "nranks must be >= 1");
-    if (nranks == 1) { *L = DistLayout{cfg->n[0], d > 1 ? cfg->n[1] : 1, d > 2 ? cfg->n[2] : 1, 0, 0, -1, false}; return FP_OK; }
+    if (nranks == 1) {
+        *L = DistLayout{cfg->n[0], 0, cfg->n[0], cfg->n[0], 0, d > 1 ? cfg->n[1] : 1, d > 2 ? cfg->n[2] : 1, 0, 0, -1, false, false};
+        return FP_OK;
+    }
     if (d < 2) return fail(FP_ERR_UNSUPPORTED, "a 1D problem does not decompose over ranks");
-    if (!is_pow2(nranks) || cfg->n[0] % nranks) return fail(FP_ERR_UNSUPPORTED, "axis 0 must split evenly over a power-of-two rank count");
+    if (cfg->n[0] < nranks) return fail(FP_ERR_UNSUPPORTED, "axis 0 has fewer planes than ranks");
     bool other_periodic = false;
     for (int a = 1; a < d; ++a) other_periodic |= cfg->bc[a] == FP_BC_PERIODIC;
-    if (other_periodic && cfg->bc[0] != FP_BC_PERIODIC)
-        return fail(FP_ERR_UNSUPPORTED, "distributed solve: with periodic axes other than 0, axis 0 must be periodic");
-    if (fft_length(cfg->bc[0], cfg->kind[0], cfg->n[0], cfg->bc[0] == FP_BC_PERIODIC && !other_periodic, false) == 0)
-        return fail(FP_ERR_UNSUPPORTED, "distributed solve: axis 0 must be on the FFT engine (power-of-two length)");
-    for (int a = 0; a < d; ++a)
-        if (cfg->bc[a] == FP_BC_NEUMANN && cfg->kind[a] == FP_GRID_REGULAR)
-            return fail(FP_ERR_UNSUPPORTED, "distributed solve: DCT-I axes (exact mean removal) not supported");
+    if (fft_length(cfg->bc[0], cfg->kind[0], cfg->n[0], cfg->bc[0] == FP_BC_PERIODIC && !other_periodic, true) == 0)
+        return fail(FP_ERR_UNSUPPORTED, "distributed solve: axis 0 must be on the FFT engine (power-of-two FFT length: "
+                                        "n = 2^k, or 2^k +- 1 for DCT-I / DST-I)");
+    // (DCT-I plans: the exact mean removal is global -- fp_dist_mean_partial + all-reduce +
+    //  fp_dist_mean_subtract, driven by the caller after phase 2)
     // forward order without axis 0: real axes descending, then periodic descending
     int r_axis = -1;
     for (int a = d - 1; a >= 1; --a) if (cfg->bc[a] == FP_BC_PERIODIC && r_axis < 0) r_axis = a;
     if (r_axis < 0 && cfg->bc[0] == FP_BC_PERIODIC) r_axis = 0;
     DistLayout l{};
-    l.a0 = cfg->n[0] / nranks;
+    l.q = cfg->n[0] / nranks;
+    l.r = cfg->n[0] % nranks;
+    l.A = l.q + (l.r ? 1 : 0);
+    l.a0 = l.q + (rank < l.r ? 1 : 0);
+    l.off0 = dist_off(l, rank);
     l.r_axis = r_axis;
     l.cpx = r_axis > 0;
+    l.wall0_cpx = l.cpx && cfg->bc[0] != FP_BC_PERIODIC;
     l.e1 = cfg->n[1];
     l.e2 = d > 2 ? cfg->n[2] : 1;
     if (r_axis == 1) l.e1 = cfg->n[1] / 2 + 1;
@@ -758,7 +773,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
     if (st != FP_OK) return st;
     if (rank < 0 || rank >= nranks) return fail(FP_ERR_VALUE, "rank out of range");
     DistLayout DL{};
-    if ((st = dist_layout(cfg, nranks, &DL)) != FP_OK) return st;
+    if ((st = dist_layout(cfg, nranks, rank, &DL)) != FP_OK) return st;
     const bool dist = nranks > 1;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -811,11 +826,30 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         if (P->r_axis < 0 && cfg->bc[0] == FP_BC_PERIODIC) P->r_axis = 0;
         order.push_back(0);
         P->a0 = DL.a0;
+        P->A = DL.A;
         P->n[0] = DL.a0;             // local extents from here on; cfg->n keeps the global ones
         P->e1 = DL.e1; P->e2 = DL.e2; P->E1 = DL.E1; P->B = DL.B; P->x_cpx = DL.cpx;
-        // send layout: axis 1 outermost -> peer q's block (axis-1 rows [qB,(q+1)B)) is contiguous
-        if (d == 3) { P->xs[0] = DL.e2; P->xs[1] = DL.a0 * DL.e2; P->xs[2] = 1; }
-        else { P->xs[0] = 1; P->xs[1] = DL.a0; }
+        P->wall0_cpx = DL.wall0_cpx;
+        // send layout: axis 1 outermost -> peer q's block (axis-1 rows [qB,(q+1)B)) is contiguous;
+        // every rank's block holds A (= max local planes) planes, so all blocks have one size
+        if (d == 3) { P->xs[0] = DL.e2; P->xs[1] = DL.A * DL.e2; P->xs[2] = 1; }
+        else { P->xs[0] = 1; P->xs[1] = DL.A; }
+        if (DL.r != 0 || !is_pow2(DL.A)) {
+            // receive layout row of global plane j: src(j) * (B * xs1) + (j - off(src)) * xs0,
+            // in the units the MID addresses (reals for the real view)
+            const long long u = DL.wall0_cpx ? 2 : 1;
+            std::vector<long long> tab((size_t)cfg->n[0]);
+            long long src = 0;
+            for (long long j = 0; j < cfg->n[0]; ++j) {
+                while (src + 1 < nranks && j >= dist_off(DL, src + 1)) ++src;
+                tab[(size_t)j] = u * (src * DL.B * P->xs[1] + (j - dist_off(DL, src)) * P->xs[0]);
+            }
+            void* dt = nullptr;
+            if (cudaMalloc(&dt, tab.size() * sizeof(long long)) != cudaSuccess) { delete P; return fail(FP_ERR_ALLOC, "cudaMalloc row table"); }
+            P->allocs.push_back(dt);
+            if (cudaMemcpy(dt, tab.data(), tab.size() * sizeof(long long), cudaMemcpyHostToDevice) != cudaSuccess) { delete P; return fail(FP_ERR_CUDA, "upload row table"); }
+            P->row_tab = (const long long*)dt;
+        }
     }
     P->middle = order.back();
     for (int a = 0; a < 3; ++a) P->cext[a] = P->n[a];
@@ -843,7 +877,9 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
     int Mx[3] = {0, 0, 0};
     for (int a = 0; a < d; ++a) {
         const bool rf = (a == P->r_axis);
-        Mx[a] = fft_length(cfg->bc[a], cfg->kind[a], cfg->n[a], rf, !dist);   // (slab phases: dense DCT-I/DST-I)
+        // (slab phases: the local DCT-I / DST-I axes on the mixed-radix / dense engines;
+        //  axis 0's MID on the FFT engine over the receive layout)
+        Mx[a] = fft_length(cfg->bc[a], cfg->kind[a], cfg->n[a], rf, !dist || a == 0);
         DevTables& T = P->tab[a];
         if (Mx[a] > 0) {
             P->fft_mask |= 1 << a;
@@ -1051,11 +1087,15 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
             else L.push_back(make_dense(t, false, mid_c, in_c, work, dst, 1));
         } else if (dist) {
             // MID over the receive layout: global axis 0 in P blocks of a0 planes
-            PassT mid = make_fft(t, OP_MID, complex_state, complex_state, B_X, B_X, 1);
+            // (a wall axis 0 on a complex state: the real kind on the real view -- real and
+            // imaginary parts are two real lines, the eigenvalue factors are real)
+            const bool rv = DL.wall0_cpx;
+            PassT mid = make_fft(t, OP_MID, complex_state && !rv, complex_state && !rv, B_X, B_X, 1);
             mid.dist_mid = true;
-            if (d == 3) { mid.fp.g.na = (int)DL.B; mid.fp.g.nb = (int)DL.e2; }
-            else { mid.fp.g.na = 1; mid.fp.g.nb = (int)DL.B; }
-            fft_tile_shape(mid.fp, P->f32, complex_state, mid.fp.g.na, mid.fp.g.nb);
+            const int pr = rv ? 2 : 1;
+            if (d == 3) { mid.fp.g.na = (int)DL.B; mid.fp.g.nb = (int)(pr * DL.e2); }
+            else { mid.fp.g.na = 1; mid.fp.g.nb = (int)(pr * DL.B); }
+            fft_tile_shape(mid.fp, P->f32, complex_state && !rv, mid.fp.g.na, mid.fp.g.nb);
             L.push_back(mid);
         } else if (Mx[t] > 0) {
             L.push_back(make_fft(t, OP_MID, complex_state, complex_state, cur, dst, 1));
@@ -1146,6 +1186,7 @@ FP_API fp_status fp_plan_info_get(const fp_plan* P, fp_plan_info* info) {
     info->num_passes = (int)P->passes.size();  // + 3 small launches when mean_fix
     info->middle_axis = P->middle;
     info->fft_axes_mask = P->fft_mask;
+    info->exact_mean = P->mean_fix ? 1 : 0;
     return FP_OK;
 }
 
@@ -1325,13 +1366,26 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
             FftPass p = T.fp;
             g.na = p.g.na; g.nb = p.g.nb;
             if (T.dist_mid) {
-                // receive layout [source rank][axis-1 block][a0 planes][axis 2]:
-                // global plane j = src * a0 + i  ->  src * (B * a0 * e2) + i * e2
-                int lg = 0;
-                while ((1LL << lg) < P->a0) ++lg;
-                g.blk_lg = lg;
-                g.in_st_hi = g.out_st_hi = P->B * P->xs[1];
-                if (lg == 0) { g.in_st = g.out_st = g.in_st_hi; }
+                // receive layout [source rank][axis-1 block][A planes][axis 2]: global plane
+                // j = off(src) + i  ->  src * (B * A * e2) + i * e2 (shift / mask when every
+                // rank holds A = 2^lg planes, else the plan's row table)
+                const long long u = P->wall0_cpx ? 2 : 1;   // real view: strides in reals
+                g.in_st_hi = g.out_st_hi = u * P->B * P->xs[1];
+                if (P->row_tab) {
+                    g.row_tab = P->row_tab;
+                } else {
+                    int lg = 0;
+                    while ((1LL << lg) < P->A) ++lg;
+                    g.blk_lg = lg;
+                    if (lg == 0) { g.in_st = g.out_st = g.in_st_hi / u; }
+                }
+                if (u == 2) {
+                    g.in_type = g.out_type = plan_type;
+                    g.in_st *= 2; g.out_st *= 2;
+                    g.in_sa *= 2; g.out_sa *= 2;
+                    g.in_sb *= 2; g.out_sb *= 2;
+                    g.pair_b = 1;
+                }
                 if (d == 3) { g.a_off = (int)(P->rank * P->B); g.a_lim = (int)P->e1; }
                 else { g.b_off = (int)(P->rank * P->B); g.b_lim = (int)P->e1; }
             }
@@ -1386,7 +1440,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
         if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("kernel launch failed: ") + cudaGetErrorString(e));
         first = false;
     }
-    if (P->mean_fix && ph_hi == 2) {
+    if (P->mean_fix && ph_hi == 2 && P->nranks == 1) {   // (distributed: fp_dist_mean_*)
         MeanPass m{};
         for (int k = 0; k < 3; ++k) { m.ext[k] = 1; m.st[k] = 0; }
         for (int a = 0; a < d; ++a) { m.ext[3 - d + a] = (int)P->n[a]; m.st[3 - d + a] = os_s[a]; }
@@ -1503,12 +1557,13 @@ FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_d
     if (st != FP_OK) return st;
     if (rank < 0 || rank >= nranks) return fail(FP_ERR_VALUE, "rank out of range");
     DistLayout L{};
-    if ((st = dist_layout(cfg, nranks, &L)) != FP_OK) return st;
+    if ((st = dist_layout(cfg, nranks, rank, &L)) != FP_OK) return st;
     std::memset(info, 0, sizeof(*info));
     info->nranks = nranks;
     info->rank = rank;
     info->local_n0 = nranks > 1 ? L.a0 : cfg->n[0];
-    info->offset0 = (int64_t)rank * info->local_n0;
+    info->offset0 = nranks > 1 ? L.off0 : 0;
+    info->pitch_n0 = nranks > 1 ? L.A : cfg->n[0];
     info->exch_n1 = nranks > 1 ? L.E1 : 0;
     info->true_n1 = nranks > 1 ? L.e1 : 0;
     info->exch_n2 = nranks > 1 ? L.e2 : 0;
@@ -1517,12 +1572,59 @@ FP_API fp_status fp_dist_layout(const fp_config* cfg, int nranks, int rank, fp_d
     info->r_axis = L.r_axis;
     const int rb = cfg->precision == FP_F32 ? 4 : 8;
     info->elem_bytes = (L.cpx ? 2 : 1) * rb;
-    info->exchange_bytes = nranks > 1 ? (size_t)L.a0 * L.E1 * L.e2 * info->elem_bytes : 0;
+    info->exchange_bytes = nranks > 1 ? (size_t)L.A * L.E1 * L.e2 * info->elem_bytes : 0;
     return FP_OK;
 }
 
 FP_API fp_status fp_plan_create_dist(const fp_config* cfg, int device, int nranks, int rank, fp_plan** plan) {
     return build_plan(cfg, device, nranks, rank, plan);
+}
+
+// exact mean removal of a distributed DCT-I plan (solver.py:224-225 over the global grid)
+static fp_status dist_mean_pass(const fp_plan* P, void* out_local, const int64_t* out_strides, MeanPass& m) {
+    if (!P || !out_local) return fail(FP_ERR_VALUE, "NULL argument");
+    const int d = P->ndim;
+    long long dense[3];
+    dense_strides(P, false, dense);
+    for (int k = 0; k < 3; ++k) { m.ext[k] = 1; m.st[k] = 0; }
+    for (int a = 0; a < d; ++a) {
+        m.ext[3 - d + a] = (int)P->n[a];
+        m.st[3 - d + a] = out_strides ? out_strides[a] : dense[a];
+    }
+    m.data = out_local;
+    return FP_OK;
+}
+
+FP_API fp_status fp_dist_mean_partial(const fp_plan* P, void* out_local, const int64_t* out_strides, void* workspace,
+                                      size_t workspace_bytes, void* stream, double* dev_sum) {
+    MeanPass m{};
+    fp_status st = dist_mean_pass(P, out_local, out_strides, m);
+    if (st != FP_OK) return st;
+    if (!dev_sum) return fail(FP_ERR_VALUE, "dev_sum is NULL");
+    if (!workspace || workspace_bytes < mean_bytes(P) || !P->mean_fix)
+        return fail(FP_ERR_VALUE, "fp_dist_mean_partial: plan without exact mean removal, or workspace too small");
+    DeviceGuard dg(P->device);
+    m.partials = (double*)workspace;
+    m.sum_out = dev_sum;
+    cudaError_t e = launch_mean_pass(m, P->f32, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("mean partial launch failed: ") + cudaGetErrorString(e));
+    return FP_OK;
+}
+
+FP_API fp_status fp_dist_mean_subtract(const fp_plan* P, void* out_local, const int64_t* out_strides,
+                                       const double* dev_total, void* stream) {
+    MeanPass m{};
+    fp_status st = dist_mean_pass(P, out_local, out_strides, m);
+    if (st != FP_OK) return st;
+    if (!dev_total) return fail(FP_ERR_VALUE, "dev_total is NULL");
+    DeviceGuard dg(P->device);
+    double N = 1.0;
+    for (int a = 0; a < P->ndim; ++a) N *= (double)P->cfg.n[a];   // global point count
+    m.mean_in = dev_total;
+    m.inv_total = 1.0 / N;
+    cudaError_t e = launch_mean_pass(m, P->f32, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(FP_ERR_CUDA, std::string("mean subtract launch failed: ") + cudaGetErrorString(e));
+    return FP_OK;
 }
 
 FP_API fp_status fp_removed_mean(const fp_plan* P, const fp_solve_info* h, double* rm) {

@@ -47,6 +47,14 @@ struct Geometry {
     // zero-initialized geometry = plain stride)
     int blk_lg;
     long long in_st_hi, out_st_hi;
+    // uneven slabs / any rank count: element j of a line at row_tab[j] (elements;
+    // the same table for in and out -- the distributed MID runs in place)
+    const long long* row_tab;
+    // real view of a complex state (distributed MID of a wall axis 0 after a periodic
+    // axis made the state complex): line ib is part (ib & 1) of complex column ib >> 1;
+    // strides are in reals, sb steps complex columns, a_/b_ offsets and limits count
+    // complex columns
+    int pair_b;
     // global index of the line axes = local + off; lines with global >= lim
     // (lim > 0) are padding (not loaded, not stored, no eigenvalue lookup)
     int a_off, a_lim, b_off, b_lim;
@@ -201,6 +209,12 @@ struct MeanPass {               // subtract the arithmetic mean (DCT-I plans)
     long long st[3];
     void* data;                 // real, plan precision
     double* partials;           // kMeanParts + 1 doubles of workspace
+    // distributed plans (slab decomposition): the mean is global --
+    //   sum_out != nullptr: only the local sum, into *sum_out (then all-reduced by the caller)
+    //   mean_in != nullptr: only the subtraction of (*mean_in) * inv_total
+    double* sum_out;
+    const double* mean_in;
+    double inv_total;
 };
 constexpr int kMeanParts = 1184;  // 8 x 148 SMs
 

@@ -7,7 +7,9 @@ exchange would slot in" (reorder.py:7-8).  This module is that exchange on
 B200s: one process per GPU, axis 0 split into slabs, and per solve
 
     phase 0  local transforms along axes d-1..1, packed into the send buffer
-             (axis 1 outermost, so every peer's block is contiguous)
+             (axis 1 outermost, so every peer's block is contiguous; any rank
+             count: axis 0 is split evenly up to one plane, every block padded
+             to the largest slab)
     all-to-all (NCCL over NVLink / NVSwitch)
     phase 1  fused forward / eigenvalue divide / inverse along the global axis 0
              (the kernel reads the receive layout directly: no unpack pass)
@@ -67,6 +69,11 @@ class NativeBackend:
         nat.check(self._lib.fp_plan_workspace_bytes(self._handle, 0, ctypes.byref(ws)))
         self._ws_strided = int(ws.value)
         self.status = t.zeros(16, dtype=t.uint8, device=self.device)
+        pinfo = nat.FpPlanInfo()
+        nat.check(self._lib.fp_plan_info_get(self._handle, ctypes.byref(pinfo)))
+        # DCT-I plans: the arithmetic mean is removed over the GLOBAL grid (solver.py:224-225)
+        self.exact_mean = bool(pinfo.exact_mean)
+        self._npts = float(np.prod(config.shape))
 
     def __del__(self):
         h = getattr(self, "_handle", None)
@@ -105,6 +112,22 @@ class NativeBackend:
 
     def backward(self, out_local):
         self._ws2 = self._call(2, None, out_local, self.send)
+
+    def local_sum(self, out_local):
+        """Sum of this rank's output slab (float64, shape (1,), on the device)."""
+        t = dv.torch()
+        s = t.zeros(1, dtype=t.float64, device=self.device)
+        ws, nws = self._workspace(True)
+        nat.check(self._lib.fp_dist_mean_partial(self._handle, out_local.data_ptr(), nat.strides_array(out_local.stride()),
+                                                 ws.data_ptr(), nws, dv.stream_handle(self.device), s.data_ptr()))
+        self._ws_mean = ws
+        return s
+
+    def subtract_mean(self, out_local, total):
+        """out_local -= total / (global point count); `total` is the all-reduced sum (device tensor)."""
+        nat.check(self._lib.fp_dist_mean_subtract(self._handle, out_local.data_ptr(), nat.strides_array(out_local.stride()),
+                                                  total.data_ptr(), dv.stream_handle(self.device)))
+        self._keep_total = total
 
     def read_status(self):
         """(raw null coefficient, non-finite flag) of this rank, as float64 tensor on the device."""
@@ -173,6 +196,10 @@ class DistributedSolverPlan:
         be.middle()
         dist.all_to_all_single(be.send, be.recv, group=self.group)
         be.backward(out_local)
+        if getattr(be, "exact_mean", False):
+            total = be.local_sum(out_local)
+            dist.all_reduce(total, op=dist.ReduceOp.SUM, group=self.group)
+            be.subtract_mean(out_local, total)
         return out_local
 
     def solve(self, rhs_local, out_local=None):
@@ -212,7 +239,8 @@ class MultiDeviceSolverPlan:
         P = len(self.devices)
         self.backends = [NativeBackend(config, P, r, self.devices[r]) for r in range(P)]
         self.info = self.backends[0].info
-        self.a0 = int(self.info.local_n0)
+        # balanced split of axis 0 (ranks may differ by one plane)
+        self.slices = [slice(int(be.info.offset0), int(be.info.offset0) + int(be.info.local_n0)) for be in self.backends]
         from .solver import _ONES_NULL_COEFF
         from .transforms import transform_pair_for
         import math
@@ -244,10 +272,10 @@ class MultiDeviceSolverPlan:
         x = t.from_numpy(np.ascontiguousarray(rhs)) if host else rhs
         if tuple(x.shape) != self.config.shape:
             raise ValueError(f"rhs extents {tuple(x.shape)} do not match config extents {self.config.shape}")
-        bes, a0 = self.backends, self.a0
+        bes = self.backends
         outs = []
         for r, be in enumerate(bes):
-            slab = x[r * a0:(r + 1) * a0].to(be.device, non_blocking=False).contiguous()
+            slab = x[self.slices[r]].to(be.device, non_blocking=False).contiguous()
             out = be.new_output()
             with t.cuda.device(be.device):
                 be.forward(slab, out)
@@ -260,6 +288,16 @@ class MultiDeviceSolverPlan:
         for r, be in enumerate(bes):
             with t.cuda.device(be.device):
                 be.backward(outs[r])
+        if bes[0].exact_mean:
+            sums = []
+            for r, be in enumerate(bes):
+                with t.cuda.device(be.device):
+                    sums.append(be.local_sum(outs[r]))
+            self._sync()
+            total = sum(float(s_.item()) for s_ in sums)
+            for r, be in enumerate(bes):
+                with t.cuda.device(be.device):
+                    be.subtract_mean(outs[r], t.tensor([total], dtype=t.float64, device=be.device))
         self._sync()
         status = [be.read_status().cpu() for be in bes]
         dc = sum(float(s_[0]) for s_ in status)

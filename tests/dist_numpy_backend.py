@@ -26,6 +26,11 @@ class NumpyBackend:
         self.rank = rank
         self.d = len(case.shape)
         self.a0 = int(info.local_n0)
+        self.A = int(info.pitch_n0)          # planes per exchange block (balanced split, padded)
+        n0 = case.axes[0].n
+        q, r = divmod(n0, nranks)
+        self.a0s = [q + (k < r) for k in range(nranks)]
+        self.offs = [k * q + min(k, r) for k in range(nranks)]
         self.E1, self.e1, self.e2, self.B = int(info.exch_n1), int(info.true_n1), int(info.exch_n2), int(info.block_n1)
         self.cpx = bool(info.exch_complex)
         self.r_axis = int(info.r_axis)
@@ -35,6 +40,7 @@ class NumpyBackend:
         self.recv = torch.zeros(nbytes, dtype=torch.uint8)
         self.dtype = np.complex128 if self.cpx else np.float64
         self.status = np.zeros(2)
+        self.exact_mean = any(a.bc == orc.NEUMANN and a.kind == orc.REGULAR for a in case.axes)
         # forward order of the local axes: real descending, then periodic descending
         axes = [a for a in range(self.d - 1, 0, -1) if case.axes[a].bc != orc.PERIODIC]
         axes += [a for a in range(self.d - 1, 0, -1) if case.axes[a].bc == orc.PERIODIC]
@@ -44,8 +50,8 @@ class NumpyBackend:
     def _view(self, buf):
         arr = buf.numpy().view(self.dtype)
         if self.d == 3:
-            return arr.reshape(self.E1, self.a0, self.e2)
-        return arr.reshape(self.E1, self.a0)
+            return arr.reshape(self.E1, self.A, self.e2)
+        return arr.reshape(self.E1, self.A)
 
     def _fwd(self, x, ax):
         a = self.case.axes[ax]
@@ -71,14 +77,14 @@ class NumpyBackend:
             x = self._fwd(x, ax)
         s = self._view(self.send)
         s[...] = 0
-        s[: self.e1] = np.swapaxes(x, 0, 1)
+        s[: self.e1, : self.a0] = np.swapaxes(x, 0, 1)
 
     def middle(self):
         case, d = self.case, self.d
         r = self._view(self.recv)
-        # [src][B][a0][e2] -> global axis 0 first: G[src*a0 + i0, i1', i2]
+        # [src][B][A][e2] -> global axis 0 first: G[off(src) + i0, i1', i2], i0 < a0(src)
         blocks = r.reshape((self.P, self.B) + r.shape[1:])
-        g = np.concatenate([np.swapaxes(blocks[s], 0, 1) for s in range(self.P)], axis=0)
+        g = np.concatenate([np.swapaxes(blocks[s][:, : self.a0s[s]], 0, 1) for s in range(self.P)], axis=0)
         k1 = self.rank * self.B + np.arange(self.B)
         valid = k1 < self.e1
         lam1 = np.zeros(self.B)
@@ -119,14 +125,20 @@ class NumpyBackend:
         else:
             g = orc.backward_1d(orc.pair(a0)[1], spec, axis=0)
         for s in range(self.P):
-            blocks[s] = np.swapaxes(g[s * self.a0:(s + 1) * self.a0], 0, 1)
+            blocks[s][:, : self.a0s[s]] = np.swapaxes(g[self.offs[s]:self.offs[s] + self.a0s[s]], 0, 1)
 
     def backward(self, out_local):
         s = self._view(self.send)
-        x = np.swapaxes(s[: self.e1], 0, 1)
+        x = np.swapaxes(s[: self.e1, : self.a0], 0, 1)
         for ax in reversed(self.order):
             x = self._inv(x, ax)
         out_local.numpy()[...] = np.real(x)
+
+    def local_sum(self, out_local):
+        return torch.tensor([float(out_local.numpy().sum())], dtype=torch.float64)
+
+    def subtract_mean(self, out_local, total):
+        out_local.numpy()[...] -= float(total[0]) / float(np.prod(self.case.shape))
 
     def read_status(self):
         return torch.tensor(self.status.copy(), dtype=torch.float64)

@@ -23,6 +23,11 @@ CASES = {
     "c5_small": orc.Case([(16, orc.TWO_PI, orc.PERIODIC)] * 3, orc.SPECTRAL),
     "dst_2d": orc.Case([(32, 1.0, orc.DIRICHLET, orc.STAGGERED), (12, 1.5, orc.DIRICHLET, orc.STAGGERED)], orc.FD2),
     "per_x_only": orc.Case([(32, 2.0, orc.PERIODIC), (8, 1.0, orc.DIRICHLET, orc.REGULAR), (6, 1.0, orc.DIRICHLET, orc.REGULAR)], orc.FD2),
+    # a wall axis 0 after periodic local axes (complex exchanged state, real-view MID)
+    "wall0_per_3d": orc.Case([(32, 1.0, orc.NEUMANN, orc.STAGGERED), (12, orc.TWO_PI, orc.PERIODIC), (10, orc.TWO_PI, orc.PERIODIC)], orc.FD2),
+    "dct1_3d": orc.Case([(33, 1.0, orc.NEUMANN, orc.REGULAR), (9, 1.0, orc.NEUMANN, orc.REGULAR), (7, 1.0, orc.NEUMANN, orc.REGULAR)], orc.FD2),
+    "per_dct1": orc.Case([(32, orc.TWO_PI, orc.PERIODIC), (9, 1.0, orc.NEUMANN, orc.REGULAR)], orc.FD2),
+    "wall0_per_2d": orc.Case([(32, 1.0, orc.DIRICHLET, orc.STAGGERED), (10, 2.0, orc.PERIODIC)], orc.SPECTRAL),
 }
 
 
@@ -59,9 +64,7 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("name", sorted(CASES))
-def test_distributed_orchestration_matches_oracle(name, world, native_lib):
+def _run(name, world):
     case = CASES[name]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -82,3 +85,15 @@ def test_distributed_orchestration_matches_oracle(name, world, native_lib):
     assert orc.relative_l2(got, want) <= 1e-12
     for r in results:
         assert r[3] == pytest.approx(rm, abs=1e-12)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_distributed_orchestration_matches_oracle(name, world, native_lib):
+    _run(name, world)
+
+
+# uneven slabs: 32 planes over 3 ranks (11, 11, 10) -- any rank count, balanced split
+@pytest.mark.parametrize("name", ["c3_small", "c4_small", "wall0_per_3d", "dst_2d", "dct1_3d"])
+def test_distributed_uneven_slabs_world3(name, native_lib):
+    _run(name, 3)

@@ -36,11 +36,11 @@ def emulate(config, P, rhs):
     from paper_1409_8116_b200.distributed import NativeBackend
 
     bes = [NativeBackend(config, P, r) for r in range(P)]
-    a0 = bes[0].local_shape[0]
     outs = []
     for r, be in enumerate(bes):
         out = be.new_output()
-        be.forward(rhs[r * a0:(r + 1) * a0].contiguous(), out)
+        off, a0 = int(be.info.offset0), int(be.info.local_n0)
+        be.forward(rhs[off:off + a0].contiguous(), out)
         outs.append(out)
     blk = bes[0].send.numel() // P
     for r in range(P):
@@ -53,6 +53,10 @@ def emulate(config, P, rhs):
             bes[s].send[r * blk:(r + 1) * blk].copy_(bes[r].recv[s * blk:(s + 1) * blk])
     for r, be in enumerate(bes):
         be.backward(outs[r])
+    if bes[0].exact_mean:   # DCT-I: the global arithmetic mean (an all-reduce between ranks)
+        total = sum(be.local_sum(outs[r]) for r, be in enumerate(bes))
+        for r, be in enumerate(bes):
+            be.subtract_mean(outs[r], total)
     torch.cuda.synchronize()
     dc = sum(float(be.read_status()[0]) for be in bes)
     nonfinite = sum(float(be.read_status()[1]) for be in bes)
@@ -69,10 +73,21 @@ SMALL = {
     # local axes on the mixed-radix engine (non-power-of-two lengths)
     "mrwall": orc.Case([(64, 1.0, orc.NEUMANN, orc.STAGGERED), (60, 1.0, orc.NEUMANN, orc.STAGGERED), (45, 2.0, orc.NEUMANN, orc.STAGGERED)], orc.FD2),
     "mrper": orc.Case([(64, orc.TWO_PI, orc.PERIODIC), (48, orc.TWO_PI, orc.PERIODIC), (30, orc.TWO_PI, orc.PERIODIC)], orc.SPECTRAL),
+    # a wall axis 0 after periodic local axes: complex exchanged state, real-view MID
+    "wall0per3d": orc.Case([(64, 1.0, orc.NEUMANN, orc.STAGGERED), (48, orc.TWO_PI, orc.PERIODIC), (30, orc.TWO_PI, orc.PERIODIC)], orc.FD2),
+    "wall0per2d": orc.Case([(64, 1.0, orc.DIRICHLET, orc.STAGGERED), (40, 2.0, orc.PERIODIC)], orc.SPECTRAL),
+    # DCT-I / DST-I (regular walls): axis 0 (n0 = 2^k +- 1) on the FFT engine's type-I MID over the
+    # receive layout, local axes on the mixed-radix / dense engines, exact global mean removal
+    "dct1": orc.Case([(65, 1.0, orc.NEUMANN, orc.REGULAR), (33, 1.0, orc.NEUMANN, orc.REGULAR), (17, 2.0, orc.NEUMANN, orc.REGULAR)], orc.FD2),
+    "dst1": orc.Case([(63, 1.0, orc.DIRICHLET, orc.REGULAR), (31, 1.0, orc.DIRICHLET, orc.REGULAR)], orc.FD2),
+    "per_dct1": orc.Case([(64, orc.TWO_PI, orc.PERIODIC), (33, 1.0, orc.NEUMANN, orc.REGULAR), (17, 1.0, orc.NEUMANN, orc.REGULAR)], orc.FD2),
+    "dct1_wall0per": orc.Case([(65, 1.0, orc.NEUMANN, orc.REGULAR), (24, orc.TWO_PI, orc.PERIODIC), (20, orc.TWO_PI, orc.PERIODIC)], orc.FD2),
+    "wall0per3d_f32": orc.Case([(64, 1.0, orc.NEUMANN, orc.STAGGERED), (32, orc.TWO_PI, orc.PERIODIC), (16, orc.TWO_PI, orc.PERIODIC)], orc.FD2, "single"),
 }
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
+# P = 3, 5, 6, 7: uneven slabs (64 planes split 22/21/21, ...) through the MID's row table
+@pytest.mark.parametrize("P", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("name", sorted(SMALL))
 def test_dist_emulated_matches_single_gpu(name, P, torch_cuda, rng):
     t = torch_cuda
@@ -113,8 +128,8 @@ def test_dist_emulated_full_size(name, P, torch_cuda):
     assert err <= 1e-12
 
 
-@pytest.mark.parametrize("P", [2, 4])
-@pytest.mark.parametrize("name", ["c3", "c4", "c5d", "mrper"])
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("name", ["c3", "c4", "c5d", "mrper", "wall0per3d"])
 def test_multi_device_wrapper_matches_single_gpu(name, P, torch_cuda, rng):
     # the single-process multi-device wrapper; ranks share cuda:0 here
     from paper_1409_8116_b200.distributed import MultiDeviceSolverPlan
