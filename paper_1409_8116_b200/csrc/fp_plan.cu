@@ -14,11 +14,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/fastpoisson_b200.h"
 #include "fp_tables.h"
@@ -182,6 +185,15 @@ struct fp_transform {
 };
 
 namespace {
+
+// NVTX ranges (header-only NVTX v3; no-ops unless a profiler is attached): one per
+// solve / phase call and one per pass, named after the pass (ncu --nvtx filters on them)
+struct NvtxRange {
+    explicit NvtxRange(const char* s) { nvtxRangePushA(s); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -1248,6 +1260,10 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                             void* const* pass_events, void* xbuf, int ph_lo, int ph_hi,
                             const Producer* prod = nullptr, const void* ovr = nullptr) {
     if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
+    static const char* const kRange[3][3] = {{"fp_solve_phase 0", "fp_solve_phases 0-1", "fp_solve"},
+                                             {"", "fp_solve_phase 1", "fp_solve_phases 1-2"},
+                                             {"", "", "fp_solve_phase 2"}};
+    NvtxRange solve_range(ph_lo >= 0 && ph_hi <= 2 && ph_lo <= ph_hi ? kRange[ph_lo][ph_hi] : "fp_solve");
     if (ovr && P->passes_ovr.empty()) return fail(FP_ERR_UNSUPPORTED, "_inv_lam override: single-GPU plans only");
     const std::vector<PassT>& PL = ovr ? P->passes_ovr : P->passes;
     const bool need_rhs = ph_lo == 0, need_out = ph_hi == 2;
@@ -1362,6 +1378,15 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
             g.out_sb = T.b >= 0 ? so[T.b] : 0;
         }
         cudaError_t e = cudaSuccess;
+        char range_name[64];
+        {
+            static const char* const kEngine[5] = {"fft", "dense", "scale", "mixed-radix", "bluestein"};
+            static const char* const kPhase[3] = {"forward", "middle", "backward"};
+            const bool mid = T.engine == EN_FFT && T.fp.op == OP_MID;
+            std::snprintf(range_name, sizeof range_name, "pass %zu: %s axis %d (%s)", i,
+                          mid ? "MID" : kPhase[T.phase % 3], T.t, kEngine[T.engine % 5]);
+        }
+        NvtxRange pass_range(range_name);
         if (T.engine == EN_FFT) {
             FftPass p = T.fp;
             g.na = p.g.na; g.nb = p.g.nb;
