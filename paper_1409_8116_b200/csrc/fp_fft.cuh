@@ -670,6 +670,107 @@ __device__ __forceinline__ cx<T> rsplit2(cx<T> zk, cx<T> zm, cx<T> tk) {
 }
 
 
+// STRIDED forward post-processing + store of a transformed tile (natural-order
+// spectrum in shared memory): real-FFT untangle / DCT-II quarter-wave twiddle per
+// quad, written straight to HBM row by row (I/O mapping: lanes across the columns)
+template <typename T, int LOGM, int OP>
+__device__ __forceinline__ void fwd_strided_post(const FftPass& p, const LineInfo& Lio, const cx<T>* line_io, int bio) {
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, HALF = S::HALF;
+    constexpr int n = 2 * M;
+    const Geometry& g = p.g;
+    const int kind = fkind_of<OP>(p);
+    const T om = (T)p.out_mult;
+    const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
+    const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
+    // thread (column, block b) owns quads q = 8 b + i, i < 8 (CFFT: k = 16 b + i):
+    //   P(q) = 8 b + (b >> 1) + i;  P(M - q) = 8 K2 - i + (i ? (K2 - 1) >> 1 : K2 >> 1), K2 = M/8 - b
+    if (Lio.valid) {
+        const long long ob = Lio.out_off;
+        const long long os = g.out_st;
+        const int b = bio;
+        const int pq0 = 8 * b + (b >> 1);
+        const int K2 = M / 8 - b;
+        const int pm0 = 8 * K2 + (K2 >> 1), pm1 = 8 * K2 + ((K2 - 1) >> 1);
+#define PM(I) ((I) == 0 ? pm0 : (pm1 - (I)))
+        if (kind == FK_CFFT) {
+            cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)(16 * b) * os;
+#pragma unroll
+            for (int it = 0; it < 16; ++it, po += os) *po = cscale<T>(line_io[17 * b + it], om);
+        } else if (kind == FK_RFFT) {
+            cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + ob;
+            cx<T>* pq = pb + (long long)(8 * b) * os;
+            cx<T>* pm = pb + (long long)(M - 8 * b) * os;
+            const T omh = om * (T)0.5;
+            QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, 8 * b, 1);   // q = 8b + it: step t_1
+#pragma unroll
+            for (int it = 0; it < 8; ++it, pq += os, pm -= os) {
+                const int q = 8 * b + it;
+                cx<T> tq, wq_unused;
+                qt.get(q, tq, wq_unused);
+                if (it == 0 && b == 0) {
+                    const cx<T> z0 = line_io[P(0)];
+                    pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
+                    pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
+                    const cx<T> zh = line_io[P(HALF)];
+                    pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
+                } else {
+                    const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
+                    *pq = cscale<T>(rsplit2<T>(zk, zm, tq), omh);
+                    *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
+                }
+            }
+        } else if (kind >= FK_DCT1) {
+            const bool d1 = kind == FK_DCT1;
+            T* const pb = reinterpret_cast<T*>(g.out) + ob;
+            const T omh = om * (T)0.5;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int q = 8 * b + it;
+                if (it == 0 && b == 0)
+                    r1_store_dc<T, M>(pb, os, d1, line_io[P(0)], line_io[P(HALF)], Wt[HALF], om, omh);
+                else
+                    r1_store_pair<T, M>(pb, os, d1, q, line_io[pq0 + it], line_io[PM(it)], Wt[q], omh);
+            }
+        } else {
+            const bool dst = kind == FK_DST2;
+            T* const pb = reinterpret_cast<T*>(g.out) + ob;
+            const long long s1 = dst ? -os : os;
+            T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;
+            T* pa = p0 + (long long)(8 * b) * s1;
+            T* pn = p0 + (long long)(n - 8 * b) * s1;
+            T* pm = p0 + (long long)(M - 8 * b) * s1;
+            T* pp = p0 + (long long)(M + 8 * b) * s1;
+            QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, 8 * b, 1);   // q = 8b + it: steps t_1, w_1
+#pragma unroll
+            for (int it = 0; it < 8; ++it, pa += s1, pn -= s1, pm -= s1, pp += s1) {
+                const int q = 8 * b + it;
+                cx<T> tq, wq;
+                qt.get(q, tq, wq);
+                if (it == 0 && b == 0) {
+                    const cx<T> z0 = line_io[P(0)];
+                    const cx<T> wM = Ww[M];
+                    p0[0] = (T)2 * (z0.x + z0.y) * om;
+                    p0[(long long)M * s1] = (T)2 * (z0.x - z0.y) * wM.x * om;
+                    const cx<T> zh = line_io[P(HALF)];
+                    const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                    p0[(long long)HALF * s1] = U.x * om;
+                    p0[(long long)(n - HALF) * s1] = -U.y * om;
+                } else {
+                    const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
+                    const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
+                    const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
+                    *pa = U1.x * om;
+                    *pn = -U1.y * om;
+                    *pm = U2.x * om;
+                    *pp = -U2.y * om;
+                }
+            }
+        }
+#undef PM
+    }
+}
+
 // ----------------------------------------------------------------------------
 // transform + post/mid/pre + store of one placed tile (contains barriers;
 // every thread of the CTA must call it).
@@ -727,92 +828,7 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
             const int kind = fkind_of<OP>(p);
             const T om = (T)p.out_mult;
             if constexpr (STRIDED) {
-                // thread (column, block b) owns quads q = 8 b + i, i < 8 (CFFT: k = 16 b + i):
-                //   P(q) = 8 b + (b >> 1) + i;  P(M - q) = 8 K2 - i + (i ? (K2 - 1) >> 1 : K2 >> 1), K2 = M/8 - b
-                if (Lio.valid) {
-                    const long long ob = Lio.out_off;
-                    const long long os = g.out_st;
-                    const int b = bio;
-                    const int pq0 = 8 * b + (b >> 1);
-                    const int K2 = M / 8 - b;
-                    const int pm0 = 8 * K2 + (K2 >> 1), pm1 = 8 * K2 + ((K2 - 1) >> 1);
-#define PM(I) ((I) == 0 ? pm0 : (pm1 - (I)))
-                    if (kind == FK_CFFT) {
-                        cx<T>* po = reinterpret_cast<cx<T>*>(g.out) + ob + (long long)(16 * b) * os;
-#pragma unroll
-                        for (int it = 0; it < 16; ++it, po += os) *po = cscale<T>(line_io[17 * b + it], om);
-                    } else if (kind == FK_RFFT) {
-                        cx<T>* const pb = reinterpret_cast<cx<T>*>(g.out) + ob;
-                        cx<T>* pq = pb + (long long)(8 * b) * os;
-                        cx<T>* pm = pb + (long long)(M - 8 * b) * os;
-                        const T omh = om * (T)0.5;
-                        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, 8 * b, 1);   // q = 8b + it: step t_1
-#pragma unroll
-                        for (int it = 0; it < 8; ++it, pq += os, pm -= os) {
-                            const int q = 8 * b + it;
-                            cx<T> tq, wq_unused;
-                            qt.get(q, tq, wq_unused);
-                            if (it == 0 && b == 0) {
-                                const cx<T> z0 = line_io[P(0)];
-                                pb[0] = mkc<T>((z0.x + z0.y) * om, 0);
-                                pb[(long long)M * os] = mkc<T>((z0.x - z0.y) * om, 0);
-                                const cx<T> zh = line_io[P(HALF)];
-                                pb[(long long)HALF * os] = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
-                            } else {
-                                const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
-                                *pq = cscale<T>(rsplit2<T>(zk, zm, tq), omh);
-                                *pm = cscale<T>(rsplit2<T>(zm, zk, t_mirror<T>(tq)), omh);
-                            }
-                        }
-                    } else if (kind >= FK_DCT1) {
-                        const bool d1 = kind == FK_DCT1;
-                        T* const pb = reinterpret_cast<T*>(g.out) + ob;
-                        const T omh = om * (T)0.5;
-#pragma unroll
-                        for (int it = 0; it < 8; ++it) {
-                            const int q = 8 * b + it;
-                            if (it == 0 && b == 0)
-                                r1_store_dc<T, M>(pb, os, d1, line_io[P(0)], line_io[P(HALF)], Wt[HALF], om, omh);
-                            else
-                                r1_store_pair<T, M>(pb, os, d1, q, line_io[pq0 + it], line_io[PM(it)], Wt[q], omh);
-                        }
-                    } else {
-                        const bool dst = kind == FK_DST2;
-                        T* const pb = reinterpret_cast<T*>(g.out) + ob;
-                        const long long s1 = dst ? -os : os;
-                        T* const p0 = dst ? pb + (long long)(n - 1) * os : pb;
-                        T* pa = p0 + (long long)(8 * b) * s1;
-                        T* pn = p0 + (long long)(n - 8 * b) * s1;
-                        T* pm = p0 + (long long)(M - 8 * b) * s1;
-                        T* pp = p0 + (long long)(M + 8 * b) * s1;
-                        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, 8 * b, 1);   // q = 8b + it: steps t_1, w_1
-#pragma unroll
-                        for (int it = 0; it < 8; ++it, pa += s1, pn -= s1, pm -= s1, pp += s1) {
-                            const int q = 8 * b + it;
-                            cx<T> tq, wq;
-                            qt.get(q, tq, wq);
-                            if (it == 0 && b == 0) {
-                                const cx<T> z0 = line_io[P(0)];
-                                const cx<T> wM = Ww[M];
-                                p0[0] = (T)2 * (z0.x + z0.y) * om;
-                                p0[(long long)M * s1] = (T)2 * (z0.x - z0.y) * wM.x * om;
-                                const cx<T> zh = line_io[P(HALF)];
-                                const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
-                                p0[(long long)HALF * s1] = U.x * om;
-                                p0[(long long)(n - HALF) * s1] = -U.y * om;
-                            } else {
-                                const cx<T> zk = line_io[pq0 + it], zm = line_io[PM(it)];
-                                const cx<T> U1 = cmul<T>(wq, rsplit2<T>(zk, zm, tq));
-                                const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(zm, zk, t_mirror<T>(tq)));
-                                *pa = U1.x * om;
-                                *pn = -U1.y * om;
-                                *pm = U2.x * om;
-                                *pp = -U2.y * om;
-                            }
-                        }
-                    }
-#undef PM
-                }
+                fwd_strided_post<T, LOGM, OP>(p, Lio, line_io, bio);
                 return;
             }
             if (Lio.valid) {

@@ -495,7 +495,10 @@ static int env_flag(const char* name, int dflt) {
     return atoi(v);
 }
 
+cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st);
+
 cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
+    if (p.tma) return launch_fft_tma(p, st);   // TMA-staged strided pass (fp_tma.cu)
     cudaError_t e = set_smem_attr();
     if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);

@@ -39,6 +39,7 @@ size_t fft_pass_smem_bytes(const FftPass& p, int real_bytes);
 int strided_line_stride(const FftPass& p, bool f32);
 cudaError_t launch_divergence(const Producer& q, void* rhs, bool f32, cudaStream_t st);
 cudaError_t launch_correct(const CorrectPass& c, bool f32, cudaStream_t st);
+bool tma_prepare(FftPass& p, bool f32);
 cudaError_t launch_blue_gather(const BluePass& p, void* S, long long l0, long long cl, bool f32, cudaStream_t st);
 cudaError_t launch_blue_emit(const BluePass& p, const void* S, long long l0, long long cl, bool f32, cudaStream_t st);
 cudaError_t launch_blue_mul(void* S, const void* bhat, long long cl, int L, bool f32, cudaStream_t st);
@@ -1427,6 +1428,7 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
             p.vec_out = (p.family == FAM_CONTIG) && g.out_st == 1 && (g.out_type == plan_type) &&
                         even_ok(g.out_sa, g.na) && even_ok(g.out_sb, g.nb) &&
                         ((uintptr_t)g.out % (2 * rb) == 0);
+            tma_prepare(p, P->f32);   // TMA-staged kernel where eligible (fp_tma.cu)
             e = launch_fft_pass(p, P->f32, st);
         } else if (T.engine == EN_MR) {
             MrPass p = T.mp;

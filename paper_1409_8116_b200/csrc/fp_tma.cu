@@ -1,0 +1,135 @@
+// fp_tma.cu -- instances and host side of the TMA-staged strided passes (fp_tma.cuh):
+// eligibility, the tensor maps (cuTensorMapEncodeTiled through the runtime's driver
+// entry point; no libcuda link), and the launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "fp_tma.cuh"
+
+namespace fpb {
+
+namespace {
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeFn) nullptr;
+        return (EncodeFn)f;
+    }();
+    return fn;
+}
+
+bool tma_enabled() {
+    static const bool on = [] { const char* v = std::getenv("FP_TMA"); return !(v && *v == '0'); }();
+    return on;
+}
+
+// 3D map over (columns b [stride 1], transform axis, a axis) of a real fp64 array;
+// dims 1 / 2 ordered by stride (tdim = the transform axis' dim).  `phase`: boxes of
+// 64 rows at traversal stride 4 (PHASE staging), else 256 consecutive rows.
+bool encode(CUtensorMap* map, const void* base, long long nb, long long nt, long long na, long long st,
+            long long sa, bool phase, int* tdim) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    const bool t_first = st <= sa || na <= 1;
+    cuuint64_t dims[3] = {(cuuint64_t)nb, (cuuint64_t)(t_first ? nt : na), (cuuint64_t)(t_first ? na : nt)};
+    cuuint64_t strides[2] = {(cuuint64_t)((t_first ? st : sa) * 8), (cuuint64_t)((t_first ? sa : st) * 8)};
+    if (na <= 1) strides[1] = strides[0] * (cuuint64_t)nt;   // (a dummy axis: any consistent stride)
+    cuuint32_t box[3] = {16, 1, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const int td = t_first ? 1 : 2;
+    box[td] = 256;
+    es[td] = phase ? 4 : 1;
+    *tdim = td;
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// per-op variant (FP_TMA_FWD / FP_TMA_INV / FP_TMA_MID): 0 = regular kernel, 1 = the
+// between-FFT step in registers + warp shuffles, 2 = through the shared-memory tile
+// (fewer registers, more resident CTAs)
+int env_mode(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+int tma_mode(int op) {
+    static const int m[3] = {env_mode("FP_TMA_FWD", 2), env_mode("FP_TMA_INV", 1), env_mode("FP_TMA_MID", 1)};
+    return m[op];
+}
+
+template <int LOGM>
+FftKernelFn tma_kernel(const FftPass& p) {
+    const bool sm = tma_mode(p.op) == 2;
+    if (p.op == OP_FWD) return sm ? fft_pass_tma<LOGM, OP_FWD, true> : fft_pass_tma<LOGM, OP_FWD>;
+    if (p.op == OP_INV) return sm ? fft_pass_tma<LOGM, OP_INV, true> : fft_pass_tma<LOGM, OP_INV>;
+    if (p.fkind == FK_DST2) return sm ? fft_pass_tma<LOGM, mid_op(FK_DST2), true> : fft_pass_tma<LOGM, mid_op(FK_DST2)>;
+    return sm ? fft_pass_tma<LOGM, mid_op(FK_DCT2), true> : fft_pass_tma<LOGM, mid_op(FK_DCT2)>;
+}
+
+FftKernelFn tma_kernel_for(const FftPass& p) {
+    switch (p.logM) {
+        case 7: return tma_kernel<7>(p);
+        case 8: return tma_kernel<8>(p);
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+// fills p.tm_in / p.tm_out and sets p.tma when the pass runs on the TMA kernel:
+// fp64 DCT-II / DST-II forward, DCT-III / DST-III inverse, or their MID, strided
+// over 16 adjacent columns (128-B rows) of plan-typed operands with 16-B aligned
+// rows, M = 128 or 256 (one 128-B row segment per line per tile)
+bool tma_prepare(FftPass& p, bool f32) {
+    p.tma = 0;
+    if (!tma_enabled() || f32 || p.family != FAM_STRIDED || p.lines != 16 || (p.logM != 7 && p.logM != 8)) return false;
+    if (tma_mode(p.op) == 0) return false;
+    const bool real_fwd = p.fkind == FK_DCT2 || p.fkind == FK_DST2;
+    const bool real_inv = p.ikind == IK_DCT3 || p.ikind == IK_DST3;
+    if ((p.op == OP_FWD && !real_fwd) || (p.op == OP_INV && !real_inv) || (p.op == OP_MID && !real_fwd)) return false;
+    const Geometry& g = p.g;
+    if (g.blk_lg > 0 || g.row_tab || g.pair_b || g.a_lim > 0 || g.b_lim > 0 || p.prod.active) return false;
+    if (g.in_type != ET_F64 || g.out_type != ET_F64) return false;
+    if ((g.nb > 1 && (g.in_sb != 1 || g.out_sb != 1)) || g.nb < 1) return false;
+    auto ok16 = [](long long s) { return (s * 8) % 16 == 0; };
+    if (!ok16(g.in_st) || !ok16(g.out_st) || (g.na > 1 && (!ok16(g.in_sa) || !ok16(g.out_sa)))) return false;
+    if (((uintptr_t)g.in % 16) || ((uintptr_t)g.out % 16)) return false;
+    const long long nreal = 2LL * p.M;
+    int td_in = 0, td_out = 0;
+    const bool phase_in = p.op != OP_INV, phase_out = p.op != OP_FWD;
+    if (!encode(&p.tm_in, g.in, g.nb, nreal, g.na, g.in_st, g.in_sa, phase_in, &td_in)) return false;
+    if (!encode(&p.tm_out, g.out, g.nb, nreal, g.na, g.out_st, g.out_sa, phase_out, &td_out)) return false;
+    if (td_in != td_out) return false;
+    p.tm_tdim = td_in;
+    p.tma = 1;
+    return true;
+}
+
+cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
+    FftKernelFn fn = tma_kernel_for(p);
+    if (!fn) return cudaErrorInvalidValue;
+    const size_t smem = tma_smem_bytes(p, (size_t)(2 * p.M) * 128);
+    static bool attr[2][3][2][2] = {};
+    bool& a = attr[p.logM - 7][p.op][p.fkind == FK_DST2][tma_mode(p.op) == 2];
+    if (!a) {
+        cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        a = true;
+    }
+    const int threads = p.lines << (p.logM - 4);
+    fn<<<p.tiles, threads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace fpb

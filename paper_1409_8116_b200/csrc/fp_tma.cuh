@@ -1,0 +1,477 @@
+// fp_tma.cuh -- TMA-staged strided passes of the FFT line engine (fp64 DCT / DST
+// lines, 16 adjacent columns = 128-B rows per tile, M <= 512: c3's y and x passes).
+//
+// The regular strided kernel moves every element through the LSU twice on the
+// way in (LDG into registers, STS into the padded tile at its Makhoul position)
+// and twice on the way out (LDS, STG); ncu put those passes at 68-70 % of the LSU
+// data pipe (profiles/r02/ncu_full_c3_strided_v2.md).  Here one thread issues
+// cp.async.bulk.tensor copies that land the tile in shared memory without the
+// LSU, and the first FFT stage reads its butterfly inputs straight out of the
+// staged rows (the Makhoul / half-FFT permutation folded into that read); the
+// last inverse stage leaves its outputs in registers, which are written in the
+// staged row layout and stored with cp.async.bulk.tensor.
+//
+// Staging layouts (SWIZZLE_128B: 16-B chunk c of row r at chunk c ^ (r & 7), so
+// 16 lanes reading one column of 16 consecutive rows hit 8 distinct chunks):
+//   PHASE   real rows y = 4t + phi in sub-tile phi, row t (TMA traversal stride 4):
+//           the Makhoul half-FFT pairs z_m = (v_2m, v_2m+1) are rows (4m, 4m+2) for
+//           m < M/2 and (2n-1-4m, 2n-3-4m) for m >= M/2 -- phases (0, 2) resp.
+//           (3, 1) at the same t -- so consecutive m are consecutive t;
+//   NATURAL rows in order (spectra: DCT-II outputs, DCT-III inputs).
+// The staging area aliases the padded FFT tile: every stage reads all of its
+// inputs before a barrier and only then writes.
+#pragma once
+#include <cuda.h>
+
+#include "fp_fft.cuh"
+
+namespace fpb {
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    unsigned done = 0;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src)) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit_wait() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// element (row r, column c) of a 1024-B aligned staging region of 128-B rows (fp64)
+__device__ __forceinline__ int stg_off(int r, int c) { return r * 128 + ((((c >> 1) ^ r) & 7) << 4) + ((c & 1) << 3); }
+
+template <int N>   // real line length n; PHASE sub-tile phi starts at phi * (n/4) rows
+__device__ __forceinline__ double& stg_phase(unsigned char* stg, int phi, int t, int c) {
+    return *reinterpret_cast<double*>(stg + phi * (N / 4) * 128 + stg_off(t, c));
+}
+__device__ __forceinline__ double& stg_nat(unsigned char* stg, int r, int c) {
+    return *reinterpret_cast<double*>(stg + stg_off(r, c));
+}
+
+// one tile's coordinates: column block start, a index
+struct TmaTile {
+    int c0, ia;
+};
+__device__ __forceinline__ TmaTile tma_tile(const FftPass& p) {
+    TmaTile t;
+    t.ia = blockIdx.x / p.nbt;
+    t.c0 = (blockIdx.x % p.nbt) * p.lines;
+    return t;
+}
+// TMA coordinates (dim 0 = columns; the transform axis is dim p.tm_tdim, the a axis the other)
+__device__ __forceinline__ void tma_coords(const FftPass& p, const TmaTile& tt, int row, int* c1, int* c2) {
+    if (p.tm_tdim == 1) { *c1 = row; *c2 = tt.ia; }
+    else { *c1 = tt.ia; *c2 = row; }
+}
+
+// issue the loads of one tile: PHASE (4 phases x n/256 boxes of 64 rows) or NATURAL (n/256 boxes of 256 rows)
+template <int N>
+__device__ __forceinline__ void tma_issue_load(const FftPass& p, const TmaTile& tt, unsigned char* stg, uint64_t* bar,
+                                               bool phase) {
+    mbar_expect_tx(bar, (unsigned)N * 128u);
+    int c1, c2;
+    if (phase) {
+#pragma unroll
+        for (int phi = 0; phi < 4; ++phi)
+#pragma unroll
+            for (int h = 0; h < N / 256; ++h) {
+                tma_coords(p, tt, phi + 256 * h, &c1, &c2);
+                tma_load_3d(stg + (phi * (N / 4) + 64 * h) * 128, &p.tm_in, tt.c0, c1, c2, bar);
+            }
+    } else {
+#pragma unroll
+        for (int h = 0; h < N / 256; ++h) {
+            tma_coords(p, tt, 256 * h, &c1, &c2);
+            tma_load_3d(stg + 256 * h * 128, &p.tm_in, tt.c0, c1, c2, bar);
+        }
+    }
+}
+template <int N>
+__device__ __forceinline__ void tma_issue_store(const FftPass& p, const TmaTile& tt, const unsigned char* stg, bool phase) {
+    int c1, c2;
+    if (phase) {
+#pragma unroll
+        for (int phi = 0; phi < 4; ++phi)
+#pragma unroll
+            for (int h = 0; h < N / 256; ++h) {
+                tma_coords(p, tt, phi + 256 * h, &c1, &c2);
+                tma_store_3d(&p.tm_out, tt.c0, c1, c2, stg + (phi * (N / 4) + 64 * h) * 128);
+            }
+    } else {
+#pragma unroll
+        for (int h = 0; h < N / 256; ++h) {
+            tma_coords(p, tt, 256 * h, &c1, &c2);
+            tma_store_3d(&p.tm_out, tt.c0, c1, c2, stg + 256 * h * 128);
+        }
+    }
+    tma_store_commit_wait();
+}
+
+// all stages, the first from registers vio[s] = z[jt + TL s], the last into them
+template <bool INV, typename T, int LOGM, bool TWP>
+__device__ __forceinline__ void fft_tile_reg_reg(cx<T>* line, int jt, const void* __restrict__ W, cx<T>* v) {
+    constexpr int REM = LOGM & 3;
+    if constexpr (REM == 0) stockham_stage<16, 0, INV, T, LOGM, true, false, TWP>(line, jt, W, v);
+    if constexpr (REM == 1) stockham_stage<2, 0, INV, T, LOGM, true>(line, jt, W, v);
+    if constexpr (REM == 2) stockham_stage<4, 0, INV, T, LOGM, true>(line, jt, W, v);
+    if constexpr (REM == 3) stockham_stage<8, 0, INV, T, LOGM, true>(line, jt, W, v);
+    constexpr int FIRST16 = REM == 0 ? 4 : REM;
+    radix16_stages_upto<FIRST16, LOGM - 4, INV, T, LOGM, TWP>(line, jt, W);
+    stockham_stage<16, LOGM - 4, INV, T, LOGM, false, true, TWP>(line, jt, W, v);
+}
+
+// Makhoul half-FFT pairs of line lf from the PHASE staging: v[s] = z_{jt + TL s}
+template <int LOGM>
+__device__ __forceinline__ bool read_makhoul(unsigned char* stg, int lf, int jt, bool dst, cx<double>* v) {
+    constexpr int M = 1 << LOGM, TL = M / 16, n = 2 * M;
+    bool bad = false;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int m = jt + TL * s;
+        double a, b;
+        if (s < 8) {   // m < M/2: rows 4m, 4m + 2
+            a = stg_phase<n>(stg, 0, m, lf);
+            b = stg_phase<n>(stg, 2, m, lf);
+        } else {       // rows 2n-1-4m, 2n-3-4m (odd: DST-II's sign flip)
+            const int t = n / 2 - 1 - m;
+            a = stg_phase<n>(stg, 3, t, lf);
+            b = stg_phase<n>(stg, 1, t, lf);
+            if (dst) { a = -a; b = -b; }
+        }
+        bad |= !(finite_t(a) && finite_t(b));
+        v[s] = mkc<double>(a, b);
+    }
+    return bad;
+}
+// ... and back: the inverse's time-domain pairs z_m = (v_2m, v_2m+1) to the x rows
+template <int LOGM>
+__device__ __forceinline__ void write_makhoul(unsigned char* stg, int lf, int jt, bool dst, double om, const cx<double>* v) {
+    constexpr int M = 1 << LOGM, TL = M / 16, n = 2 * M;
+    const double oo = dst ? -om : om;   // DST-III: odd rows negated
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int m = jt + TL * s;
+        if (s < 8) {
+            stg_phase<n>(stg, 0, m, lf) = v[s].x * om;
+            stg_phase<n>(stg, 2, m, lf) = v[s].y * om;
+        } else {
+            const int t = n / 2 - 1 - m;
+            stg_phase<n>(stg, 3, t, lf) = v[s].x * oo;
+            stg_phase<n>(stg, 1, t, lf) = v[s].y * oo;
+        }
+    }
+}
+
+// smem layout of a TMA tile: [line table][pad to 1024][max(padded tile, staging)][mbarrier]
+template <int LOGM>
+__host__ __device__ constexpr size_t tma_stage_bytes() { return (size_t)(2 << LOGM) * 128; }
+__host__ __device__ inline size_t tma_region_bytes(const FftPass& p, size_t stage) {
+    const size_t tile = (size_t)p.lines * p.ls * 16;
+    return tile > stage ? tile : stage;
+}
+__host__ __device__ inline size_t tma_smem_bytes(const FftPass& p, size_t stage) {
+    return linfo_bytes(p.lines) + 1024 + tma_region_bytes(p, stage) + 16;
+}
+
+// OP: OP_FWD (DCT-II / DST-II lines), OP_INV (DCT-III / DST-III), or the kind-specialised MID (DCT-II / DST-II)
+// SMEM: the step between the forward and inverse FFTs goes through the shared-memory
+// tile instead of registers + warp shuffles (fewer registers -> 3 CTAs per SM):
+//   forward: post-process from the spectrum in shared memory, row stores to HBM;
+//   inverse: pre-processed spectrum written to the tile, then the inverse FFT;
+//   MID:     forward FFT into the tile, the folded 1/lam step in place per quad, inverse FFT
+// (register paths: two resident CTAs, <= 128 registers -- an explicit minimum of 1 lets
+// ptxas take 220+ and drops to one CTA per SM; shared-memory variants: three CTAs, 80
+// registers -- the forward fits with 8 B of spill, the MID / inverse spill more and
+// measured slower than their register paths, profiles/r02/ab_tma_variants.txt)
+template <int LOGM, int OP, bool SMEM = false>
+__global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_constant__ FftPass p) {
+    using T = double;
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, n = 2 * M;
+    constexpr size_t STG = tma_stage_bytes<LOGM>();
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // (the staging base is aligned to 1024 below)
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(smem_raw + linfo_bytes(p.lines));
+    unsigned char* stg = reinterpret_cast<unsigned char*>((b0 + 1023) & ~(uintptr_t)1023);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(stg);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + tma_region_bytes(p, STG));
+    const int tid = threadIdx.x;
+    const TmaTile tt = tma_tile(p);
+    constexpr bool kFwdIn = opb(OP) != OP_INV;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        tma_issue_load<n>(p, tt, stg, bar, kFwdIn);
+    }
+    setup_lines<true, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+
+    const int lf = tid >> LOGTL, jt = tid & (TL - 1);
+    const int lane = tid & 31;
+    const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
+    const int LS = line_stride<T, LOGM, true>(p);
+    cx<T>* line_f = sm + lf * LS;
+    const void* __restrict__ W = p.wfft;
+    const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
+    const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
+    const LineInfo L = linfo[lf];
+    cx<T> v[16], pz[8];
+    mbar_wait(bar, 0);
+
+    if constexpr (opb(OP) == OP_FWD && SMEM) {
+        const bool bad = read_makhoul<LOGM>(stg, lf, jt, p.fkind == FK_DST2, v);
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        fft_tile_from_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        const int lio = tid & (p.lines - 1), bio = tid >> p.logLines;
+        fwd_strided_post<T, LOGM, OP>(p, linfo[lio], sm + lio * LS, bio);
+        return;
+    } else if constexpr (opb(OP) == OP_FWD) {
+        const bool dst = p.fkind == FK_DST2;
+        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        fetch_mirror<T>(v, pz, jt, partner);
+        __syncthreads();   // every thread is done with the tile: the staging may be overwritten
+        // DCT-II quads {q, n-q, M-q, M+q} into NATURAL rows (DST-II: row n-1-k)
+        const T om = (T)p.out_mult;
+        auto row = [&](int k) { return dst ? n - 1 - k : k; };
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq;
+            qt.get(q, tq, wq);
+            if (r == 0 && jt == 0) {
+                const cx<T> z0 = v[0], zh = v[8];
+                const cx<T> wM = Ww[M];
+                stg_nat(stg, row(0), lf) = (T)2 * (z0.x + z0.y) * om;
+                stg_nat(stg, row(M), lf) = (T)2 * (z0.x - z0.y) * wM.x * om;
+                const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                stg_nat(stg, row(HALF), lf) = U.x * om;
+                stg_nat(stg, row(n - HALF), lf) = -U.y * om;
+            } else {
+                const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
+                const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)));
+                stg_nat(stg, row(q), lf) = U1.x * om;
+                stg_nat(stg, row(n - q), lf) = -U1.y * om;
+                stg_nat(stg, row(M - q), lf) = U2.x * om;
+                stg_nat(stg, row(M + q), lf) = -U2.y * om;
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) tma_issue_store<n>(p, tt, stg, false);
+        return;
+    } else if constexpr (opb(OP) == OP_INV && SMEM) {
+        const bool dst = p.ikind == IK_DST3;
+        auto X = [&](int k) { return stg_nat(stg, dst ? n - 1 - k : k, lf); };
+        // all spectrum values of this thread's quads first (the tile aliases the staging)
+        T xa[8], xb[8], xc[8], xd[8];
+        bool bad = false;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            if (r == 0) {   // (jt == 0: X_0, X_M, X_HALF, X_{n-HALF})
+                xa[0] = X(jt == 0 ? 0 : q);
+                xb[0] = X(jt == 0 ? M : n - q);
+                xc[0] = X(jt == 0 ? HALF : M - q);
+                xd[0] = X(jt == 0 ? n - HALF : M + q);
+            } else {
+                xa[r] = X(q); xb[r] = X(n - q); xc[r] = X(M - q); xd[r] = X(M + q);
+            }
+            bad |= !(finite_t(xa[r]) && finite_t(xb[r]) && finite_t(xc[r]) && finite_t(xd[r]));
+        }
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        __syncthreads();
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq;
+            qt.get(q, tq, wq);
+            if (r == 0 && jt == 0) {
+                const cx<T> wM = Ww[M];
+                const cx<T> VM = cmulc<T>(mkc<T>(xb[0], -xb[0]), wM);
+                line_f[P(0)] = rmerge<T>(mkc<T>(xa[0], 0), VM, mkc<T>(1, 0));
+                const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                const cx<T> Vh = cmulc<T>(mkc<T>(xc[0], -xd[0]), wh);
+                line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
+            } else {
+                const cx<T> wm = w_mirror<T>(wq), tm = t_mirror<T>(tq);
+                const cx<T> Vk = cmulc<T>(mkc<T>(xa[r], -xb[r]), wq);
+                const cx<T> Vm = cmulc<T>(mkc<T>(xc[r], -xd[r]), wm);
+                line_f[P(q)] = rmerge<T>(Vk, Vm, tq);
+                line_f[P(M - q)] = rmerge<T>(Vm, Vk, tm);
+            }
+        }
+        __syncthreads();
+        fft_tile_to_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+        write_makhoul<LOGM>(stg, lf, jt, dst, p.out_mult, v);
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) tma_issue_store<n>(p, tt, stg, true);
+        return;
+    } else if constexpr (opb(OP) == OP_INV) {
+        // DCT-III / DST-III pre-processing straight from the NATURAL staging (DST-III: X reversed)
+        const bool dst = p.ikind == IK_DST3;
+        auto X = [&](int k) { return stg_nat(stg, dst ? n - 1 - k : k, lf); };
+        cx<T> half0 = mkc<T>(0, 0);
+        bool bad = false;
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq;
+            qt.get(q, tq, wq);
+            if (r == 0 && jt == 0) {
+                const T X0 = X(0), XM = X(M), Xh = X(HALF), Xnh = X(n - HALF);
+                bad |= !(finite_t(X0) && finite_t(XM) && finite_t(Xh) && finite_t(Xnh));
+                const cx<T> wM = Ww[M];
+                const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                const cx<T> Vh = cmulc<T>(mkc<T>(Xh, -Xnh), wh);
+                half0 = rmerge<T>(Vh, Vh, th);
+            } else {
+                const T a = X(q), b = X(n - q), c = X(M - q), d = X(M + q);
+                bad |= !(finite_t(a) && finite_t(b) && finite_t(c) && finite_t(d));
+                const cx<T> wm = w_mirror<T>(wq), tm = t_mirror<T>(tq);
+                const cx<T> Vk = cmulc<T>(mkc<T>(a, -b), wq);
+                const cx<T> Vm = cmulc<T>(mkc<T>(c, -d), wm);
+                v[r] = rmerge<T>(Vk, Vm, tq);
+                pz[r] = rmerge<T>(Vm, Vk, tm);
+            }
+        }
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        return_mirror<T>(v, pz, jt, partner, half0);
+        fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+        write_makhoul<LOGM>(stg, lf, jt, dst, p.out_mult, v);
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) tma_issue_store<n>(p, tt, stg, true);
+        return;
+    } else if constexpr (SMEM) {
+        // MID through the tile: forward FFT (first stage from the staging) into shared memory,
+        // the folded 1/lam step in place per quad (each quad's two slots belong to one thread),
+        // inverse FFT with its last stage into registers
+        const int kind = fkind_of<OP>(p);
+        const bool dst = kind == FK_DST2;
+        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        fft_tile_from_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        const Scaling& Sc = p.s;
+        const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+#define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
+        const cx<T>* __restrict__ Wb = reinterpret_cast<const cx<T>*>(p.wb);
+        const double* __restrict__ lt = Sc.lam_t;
+        const double C = line_lam_sum(L);
+        auto quad = [&](int q) {
+            cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
+            mid_quad<T>(zk, zm, Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C), eig_recip_nz<T>(lt, KPHYS(n - q), C),
+                        eig_recip_nz<T>(lt, KPHYS(M - q), C), eig_recip_nz<T>(lt, KPHYS(M + q), C));
+            line_f[P(q)] = zk;
+            line_f[P(M - q)] = zm;
+        };
+        if (jt == 0) {
+            const cx<T> z0 = line_f[P(0)];
+            const cx<T> wM = Ww[M];
+            T X0 = (T)2 * (z0.x + z0.y);
+            T XM = (T)2 * (z0.x - z0.y) * wM.x;
+            if (cap && !dst) *Sc.dc_out = (double)X0;
+            X0 *= eig_recip<T>(lt, KPHYS(0), C);
+            XM *= eig_recip<T>(lt, KPHYS(M), C);
+            const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+            line_f[P(0)] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+            const cx<T> zh = line_f[P(HALF)];
+            const cx<T> wh = Ww[HALF], th = Wt[HALF];
+            const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
+            const T Xa = (T)2 * U.x * eig_recip<T>(lt, KPHYS(HALF), C);
+            const T Xb = (T)-2 * U.y * eig_recip<T>(lt, KPHYS(n - HALF), C);
+            const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
+            line_f[P(HALF)] = rmerge<T>(Vh, Vh, th);
+        } else {
+            quad(jt);
+        }
+#pragma unroll 1
+        for (int it = 1; it < 8; ++it) quad(jt + it * TL);
+#undef KPHYS
+        __syncthreads();
+        fft_tile_to_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+        write_makhoul<LOGM>(stg, lf, jt, dst, p.out_mult * Sc.bscale * Sc.inv_np, v);
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) tma_issue_store<n>(p, tt, stg, true);
+    } else {
+        // MID: forward, null capture, folded 1/lam step, inverse -- all in registers but the FFT stages
+        const int kind = fkind_of<OP>(p);
+        const bool dst = kind == FK_DST2;
+        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        const Scaling& Sc = p.s;
+        const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+        fetch_mirror<T>(v, pz, jt, partner);
+        cx<T> half0 = mkc<T>(0, 0);
+#define KPHYS(K) (dst ? (n - 1 - (K)) : (K))
+        const cx<T>* __restrict__ Wb = reinterpret_cast<const cx<T>*>(p.wb);
+        const double* __restrict__ lt = Sc.lam_t;
+        const double C = line_lam_sum(L);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            if (r == 0 && jt == 0) {
+                const cx<T> z0 = v[0], zh = v[8];
+                const cx<T> wM = Ww[M];
+                T X0 = (T)2 * (z0.x + z0.y);
+                T XM = (T)2 * (z0.x - z0.y) * wM.x;
+                if (cap && !dst) *Sc.dc_out = (double)X0;
+                X0 *= eig_recip<T>(lt, KPHYS(0), C);
+                XM *= eig_recip<T>(lt, KPHYS(M), C);
+                const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                const cx<T> U = cmul<T>(wh, rsplit<T>(zh, zh, th));
+                const T Xa = (T)2 * U.x * eig_recip<T>(lt, KPHYS(HALF), C);
+                const T Xb = (T)-2 * U.y * eig_recip<T>(lt, KPHYS(n - HALF), C);
+                const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
+                half0 = rmerge<T>(Vh, Vh, th);
+            } else {
+                mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C),
+                            eig_recip_nz<T>(lt, KPHYS(n - q), C), eig_recip_nz<T>(lt, KPHYS(M - q), C),
+                            eig_recip_nz<T>(lt, KPHYS(M + q), C));
+            }
+        }
+#undef KPHYS
+        return_mirror<T>(v, pz, jt, partner, half0);
+        fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+        write_makhoul<LOGM>(stg, lf, jt, dst, p.out_mult * Sc.bscale * Sc.inv_np, v);
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) tma_issue_store<n>(p, tt, stg, true);
+    }
+}
+
+}  // namespace fpb

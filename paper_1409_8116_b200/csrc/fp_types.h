@@ -9,6 +9,7 @@
 //   MID  forward -> eigenvalue scale -> inverse along the last forward axis,
 //        with null-mode capture (solver.py:216-223), all on one on-chip tile.
 #pragma once
+#include <cuda.h>   // CUtensorMap (type only; the maps are encoded through the runtime's driver entry point)
 #include <stdint.h>
 
 namespace fpb {
@@ -108,6 +109,10 @@ struct FftPass {
     Producer prod;              // first pass of a fused projection step (active = 0 otherwise)
     int sub;                    // STRIDED MID: compute sub-tiles per I/O tile (0/1 = one; 2 = the
                                 // tile is twice as wide as one 512-thread compute pass)
+    // TMA-staged strided pass (fp_tma.cu): tensor maps of the in / out arrays, filled at
+    // solve time by tma_prepare; tm_tdim = the map dimension of the transform axis
+    int tma, tm_tdim;
+    CUtensorMap tm_in, tm_out;
 };
 
 struct DensePass {

@@ -145,9 +145,13 @@ def test_status_codes(lib):
     cfg = make_cfg(CASES["neu3d"])
     h = ctypes.c_void_p()
     assert lib.fp_plan_create(ctypes.byref(cfg), 99, ctypes.byref(h)) == nat.FP_ERR_VALUE
-    cfg.n[0] = 5000 * 3 + 1  # odd, > dense limit, not on the FFT engine
+    cfg.n[0] = 5000 * 3 + 1  # odd, above the dense limit, not on the FFT engine: Bluestein (used to be unsupported)
     cfg.bc[0] = nat.FP_BC_DIRICHLET
     cfg.kind[0] = nat.FP_GRID_REGULAR
     cfg.bc[1] = cfg.bc[2] = nat.FP_BC_DIRICHLET
     cfg.kind[1] = cfg.kind[2] = nat.FP_GRID_REGULAR
-    assert lib.fp_plan_create(ctypes.byref(cfg), 0, ctypes.byref(h)) == nat.FP_ERR_UNSUPPORTED
+    assert lib.fp_plan_create(ctypes.byref(cfg), 0, ctypes.byref(h)) == nat.FP_OK, lib.fp_last_error()
+    lib.fp_plan_destroy(h)
+    # a slab decomposition needs axis 0 on the FFT engine: 15001 points -> FP_ERR_UNSUPPORTED
+    assert lib.fp_plan_create_dist(ctypes.byref(cfg), 0, 2, 0, ctypes.byref(h)) == nat.FP_ERR_UNSUPPORTED
+    assert b"FFT engine" in lib.fp_last_error()

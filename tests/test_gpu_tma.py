@@ -1,0 +1,76 @@
+"""GPU tier: the TMA-staged strided passes (csrc/fp_tma.cuh) -- fp64 DCT / DST lines of
+256 and 512 points over 16-column tiles: the forward pass, the MID and the inverse pass
+on the cp.async.bulk.tensor path, including ragged column counts (the last tile's
+columns out of bounds: zero-filled loads, clipped stores), a missing line axis (2D),
+the first pass's non-finite check, and strided operands that are not eligible (they
+fall back to the regular kernel).  Results against the oracle (solver.py:191-249).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1409_8116_b200 as fp
+from paper_1409_8116_b200.grid import Approximation as AP, BoundaryCondition as BC, GridKind as GK
+from oracle import fastpoisson_oracle as orc
+
+pytestmark = pytest.mark.gpu
+N_, D_, P_, S_ = orc.NEUMANN, orc.DIRICHLET, orc.PERIODIC, orc.STAGGERED
+
+CASES = {
+    "mid512_2d": orc.Case([(512, 1.0, N_, S_), (40, 1.5, N_, S_)], orc.FD2),
+    "mid256_dst_2d": orc.Case([(256, 1.0, D_, S_), (100, 2.0, D_, S_)], orc.FD2),
+    "fwd_inv512_3d": orc.Case([(24, 1.0, N_, S_), (512, 1.0, N_, S_), (33, 2.0, N_, S_)], orc.FD2),
+    "mid_fwd256_3d": orc.Case([(256, 1.0, D_, S_), (256, 1.0, D_, S_), (20, 1.0, D_, S_)], orc.FD2),
+    "wall_first_pass": orc.Case([(512, 1.0, N_, S_), (48, orc.TWO_PI, P_), (32, orc.TWO_PI, P_)], orc.SPECTRAL),
+    "c3_quarter": orc.Case([(128, 1.0, N_, S_), (256, 1.0, N_, S_), (512, 1.0, N_, S_)], orc.FD2),
+    "dst_c3_like": orc.Case([(256, 1.0, D_, S_), (512, 1.0, D_, S_), (64, 1.0, D_, S_)], orc.SPECTRAL),
+}
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _config(case):
+    grids = tuple(fp.GridSpec(a.n, a.length, BC(a.bc), GK(a.kind)) for a in case.axes)
+    return fp.SolverConfig(grids, AP(case.approx), case.precision)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_tma_passes_match_oracle(name, torch_cuda, rng):
+    case = CASES[name]
+    rhs = rng.standard_normal(case.shape)
+    want, rm = orc.solve(case, rhs)
+    plan = fp.SolverPlan(_config(case))
+    got, rep = plan.solve(rhs)
+    assert orc.relative_l2(got, want) <= 1e-12
+    assert rep.removed_mean == pytest.approx(rm, abs=1e-12)
+    # device tensors, in place
+    x = torch_cuda.from_numpy(rhs).cuda()
+    plan.solve(x, out=x)
+    assert orc.relative_l2(x.cpu().numpy(), want) <= 1e-12
+
+
+def test_tma_first_pass_nonfinite(torch_cuda, rng):
+    case = CASES["wall_first_pass"]
+    rhs = rng.standard_normal(case.shape)
+    rhs[300, 7, 5] = np.nan
+    with pytest.raises(ValueError):
+        fp.SolverPlan(_config(case)).solve(rhs)
+
+
+def test_tma_ineligible_strides_fall_back(torch_cuda, rng):
+    # a ghost-cell sub-block: rows 8-B aligned only -> the regular strided kernel
+    t = torch_cuda
+    case = CASES["mid512_2d"]
+    big = t.from_numpy(rng.standard_normal((514, 42))).cuda()
+    want, _ = orc.solve(case, big[1:-1, 1:-1].cpu().numpy())
+    out = t.zeros_like(big)
+    fp.SolverPlan(_config(case)).solve(big[1:-1, 1:-1], out=out[1:-1, 1:-1])
+    assert orc.relative_l2(out[1:-1, 1:-1].cpu().numpy(), want) <= 1e-12
+    assert float(out[0].abs().max()) == 0.0 and float(out[:, 0].abs().max()) == 0.0
