@@ -211,8 +211,11 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
     constexpr size_t STG = tma_stage_bytes<LOGM>();
     extern __shared__ __align__(16) unsigned char smem_raw[];   // (the staging base is aligned to 1024 below)
     LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
-    const uintptr_t b0 = reinterpret_cast<uintptr_t>(smem_raw + linfo_bytes(p.lines));
-    unsigned char* stg = reinterpret_cast<unsigned char*>((b0 + 1023) & ~(uintptr_t)1023);
+    // 1024-B aligned staging (SWIZZLE_128B); offset arithmetic on the __shared__ array keeps
+    // the compiler on LDS/STS (an integer round trip of the address would turn every tile
+    // access into a generic LD/ST)
+    unsigned char* const b0 = smem_raw + linfo_bytes(p.lines);
+    unsigned char* stg = b0 + ((1024u - (smem_addr(b0) & 1023u)) & 1023u);
     cx<T>* sm = reinterpret_cast<cx<T>*>(stg);
     uint64_t* bar = reinterpret_cast<uint64_t*>(stg + tma_region_bytes(p, STG));
     const int tid = threadIdx.x;
