@@ -424,6 +424,15 @@ def run_dist(args, ws, rank, local):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     elapsed_ms = float(tt.item())
     ms_step = elapsed_ms / args.steps
+    # per-phase breakdown (a second, untimed pass: events between the phases and exchanges)
+    ph_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
+    for k in range(args.steps):
+        plan.solve_async(rhs, out, events=ph_ev[k])
+    torch.cuda.synchronize(dev)
+    ph = torch.tensor([[e[j].elapsed_time(e[j + 1]) for j in range(5)] for e in ph_ev], device=dev,
+                      dtype=torch.float64).mean(dim=0)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+    phase_ms = [float(x) for x in ph.tolist()]
     value = args.steps / (elapsed_ms * 1e-3)          # solves/s of the one global grid
     hbm_peak, peak_src = peaks()
     import ctypes
@@ -444,6 +453,23 @@ def run_dist(args, ws, rank, local):
         "nvlink": {"bytes_per_gpu_per_solve": nvl_bytes, "achieved": nvl_bytes / (ms_step * 1e-3) / 1e9,
                    "peak": nvl_peak, "unit": "GB/s", "frac": nvl_bytes / (ms_step * 1e-3) / 1e9 / nvl_peak,
                    "peak_source": "nominal NVLink 5 per direction per GPU"},
+    }
+    # phases (max over ranks of the per-rank means): local forward passes, exchange, MID,
+    # exchange back, local inverse passes -- the compute phases against HBM, the exchanges
+    # against NVLink (each moves (P-1)/P of the exchange buffer per direction)
+    n_local = (len(shape) - 1)
+    x_one = xbytes * (ws - 1) / ws
+    loc_bytes = 2 * n_pts * s / ws
+    roofline["phases"] = {
+        "names": ["forward (local axes)", "all-to-all", "MID (axis 0)", "all-to-all back", "backward (local axes)"],
+        "ms": phase_ms,
+        "hbm_frac": [n_local * loc_bytes / (phase_ms[0] * 1e-3) / 1e9 / hbm_peak, None,
+                     loc_bytes / (phase_ms[2] * 1e-3) / 1e9 / hbm_peak, None,
+                     n_local * loc_bytes / (phase_ms[4] * 1e-3) / 1e9 / hbm_peak],
+        "nvlink_frac": [None, x_one / (phase_ms[1] * 1e-3) / 1e9 / nvl_peak, None,
+                        x_one / (phase_ms[3] * 1e-3) / 1e9 / nvl_peak, None],
+        "how": "CUDA events on the compute stream between the phases of K extra solves; the exchanges "
+               "are torch.distributed.all_to_all_single (NCCL), ordered on that stream",
     }
     # e2e: each rank's slab from pinned host memory, solve, slab back (public distributed API)
     e2e = None

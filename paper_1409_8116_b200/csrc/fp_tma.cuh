@@ -142,9 +142,8 @@ __device__ __forceinline__ void fft_tile_reg_reg(cx<T>* line, int jt, const void
 
 // Makhoul half-FFT pairs of line lf from the PHASE staging: v[s] = z_{jt + TL s}
 template <int LOGM>
-__device__ __forceinline__ bool read_makhoul(unsigned char* stg, int lf, int jt, bool dst, cx<double>* v) {
+__device__ __forceinline__ void read_makhoul(unsigned char* stg, int lf, int jt, bool dst, cx<double>* v) {
     constexpr int M = 1 << LOGM, TL = M / 16, n = 2 * M;
-    bool bad = false;
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
         const int m = jt + TL * s;
@@ -158,11 +157,20 @@ __device__ __forceinline__ bool read_makhoul(unsigned char* stg, int lf, int jt,
             b = stg_phase<n>(stg, 1, t, lf);
             if (dst) { a = -a; b = -b; }
         }
-        bad |= !(finite_t(a) && finite_t(b));
         v[s] = mkc<double>(a, b);
     }
+}
+// the first pass's non-finite check (solver.py:201-202) of line lf: this thread's 2M/TL
+// staged values of its column (every row of a line is covered by its TL threads)
+template <int LOGM>
+__device__ __forceinline__ bool staged_nonfinite(unsigned char* stg, int lf, int jt) {
+    constexpr int M = 1 << LOGM, TL = M / 16, n = 2 * M;
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < n / TL; ++i) bad |= !finite_t(*reinterpret_cast<const double*>(stg + stg_off(jt + TL * i, lf)));
     return bad;
 }
+
 // ... and back: the inverse's time-domain pairs z_m = (v_2m, v_2m+1) to the x rows
 template <int LOGM>
 __device__ __forceinline__ void write_makhoul(unsigned char* stg, int lf, int jt, bool dst, double om, const cx<double>* v) {
@@ -241,16 +249,16 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
     mbar_wait(bar, 0);
 
     if constexpr (opb(OP) == OP_FWD && SMEM) {
-        const bool bad = read_makhoul<LOGM>(stg, lf, jt, p.fkind == FK_DST2, v);
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        read_makhoul<LOGM>(stg, lf, jt, p.fkind == FK_DST2, v);
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         fft_tile_from_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         const int lio = tid & (p.lines - 1), bio = tid >> p.logLines;
         fwd_strided_post<T, LOGM, OP>(p, linfo[lio], sm + lio * LS, bio);
         return;
     } else if constexpr (opb(OP) == OP_FWD) {
         const bool dst = p.fkind == FK_DST2;
-        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         fetch_mirror<T>(v, pz, jt, partner);
         __syncthreads();   // every thread is done with the tile: the staging may be overwritten
@@ -289,7 +297,6 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
         auto X = [&](int k) { return stg_nat(stg, dst ? n - 1 - k : k, lf); };
         // all spectrum values of this thread's quads first (the tile aliases the staging)
         T xa[8], xb[8], xc[8], xd[8];
-        bool bad = false;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int q = jt + r * TL;
@@ -301,9 +308,8 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
             } else {
                 xa[r] = X(q); xb[r] = X(n - q); xc[r] = X(M - q); xd[r] = X(M + q);
             }
-            bad |= !(finite_t(xa[r]) && finite_t(xb[r]) && finite_t(xc[r]) && finite_t(xd[r]));
         }
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         __syncthreads();
         QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
 #pragma unroll
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
         const bool dst = p.ikind == IK_DST3;
         auto X = [&](int k) { return stg_nat(stg, dst ? n - 1 - k : k, lf); };
         cx<T> half0 = mkc<T>(0, 0);
-        bool bad = false;
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -348,7 +354,6 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
             qt.get(q, tq, wq);
             if (r == 0 && jt == 0) {
                 const T X0 = X(0), XM = X(M), Xh = X(HALF), Xnh = X(n - HALF);
-                bad |= !(finite_t(X0) && finite_t(XM) && finite_t(Xh) && finite_t(Xnh));
                 const cx<T> wM = Ww[M];
                 const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
                 v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
@@ -357,7 +362,6 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
                 half0 = rmerge<T>(Vh, Vh, th);
             } else {
                 const T a = X(q), b = X(n - q), c = X(M - q), d = X(M + q);
-                bad |= !(finite_t(a) && finite_t(b) && finite_t(c) && finite_t(d));
                 const cx<T> wm = w_mirror<T>(wq), tm = t_mirror<T>(tq);
                 const cx<T> Vk = cmulc<T>(mkc<T>(a, -b), wq);
                 const cx<T> Vm = cmulc<T>(mkc<T>(c, -d), wm);
@@ -365,7 +369,6 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
                 pz[r] = rmerge<T>(Vm, Vk, tm);
             }
         }
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
         return_mirror<T>(v, pz, jt, partner, half0);
         fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         __syncthreads();
@@ -380,8 +383,8 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
         // inverse FFT with its last stage into registers
         const int kind = fkind_of<OP>(p);
         const bool dst = kind == FK_DST2;
-        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         fft_tile_from_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         const Scaling& Sc = p.s;
         const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
@@ -430,8 +433,8 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
         // MID: forward, null capture, folded 1/lam step, inverse -- all in registers but the FFT stages
         const int kind = fkind_of<OP>(p);
         const bool dst = kind == FK_DST2;
-        const bool bad = read_makhoul<LOGM>(stg, lf, jt, dst, v);
-        if (bad && p.nonfinite && L.valid) *p.nonfinite = 1;
+        read_makhoul<LOGM>(stg, lf, jt, dst, v);
+        if (p.nonfinite && L.valid && staged_nonfinite<LOGM>(stg, lf, jt)) *p.nonfinite = 1;
         fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         const Scaling& Sc = p.s;
         const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;

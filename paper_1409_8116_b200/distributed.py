@@ -179,9 +179,15 @@ class DistributedSolverPlan:
         self._np = math.prod(g.n for g in config.grids if g.bc.value == "periodic")
         self._null = math.prod(_ONES_NULL_COEFF[p.forward](g.n) for g, p in zip(config.grids, pairs)) if config.singular else 1.0
 
-    def solve_async(self, rhs_local, out_local=None):
-        """Enqueue one distributed solve (kernels + NCCL all-to-alls) without synchronizing."""
+    def solve_async(self, rhs_local, out_local=None, events=None):
+        """Enqueue one distributed solve (kernels + NCCL all-to-alls) without synchronizing.
+        `events`: six CUDA events recorded on the current stream around phase 0, the
+        first exchange, the MID, the second exchange and phase 2 (per-phase timing)."""
         import torch.distributed as dist
+
+        def mark(k):
+            if events is not None:
+                events[k].record()
 
         if tuple(rhs_local.shape) != self.local_shape:
             raise ValueError(f"local rhs extents {tuple(rhs_local.shape)} do not match {self.local_shape}")
@@ -191,11 +197,17 @@ class DistributedSolverPlan:
         if out_local is None:
             out_local = self.backend.new_output()
         be = self.backend
+        mark(0)
         be.forward(rhs_local, out_local)
+        mark(1)
         dist.all_to_all_single(be.recv, be.send, group=self.group)
+        mark(2)
         be.middle()
+        mark(3)
         dist.all_to_all_single(be.send, be.recv, group=self.group)
+        mark(4)
         be.backward(out_local)
+        mark(5)
         if getattr(be, "exact_mean", False):
             total = be.local_sum(out_local)
             dist.all_reduce(total, op=dist.ReduceOp.SUM, group=self.group)
