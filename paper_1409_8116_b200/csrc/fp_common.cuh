@@ -359,6 +359,17 @@ __device__ __forceinline__ T eig_recip_nz(const double* __restrict__ lam_t, int 
     const double r = recip_f64(lam);
     return (T)r;
 }
+// the four factors of a folded-MID quad from the pair table: (q, n-q) and (M-q, M+q)
+template <typename T>
+__device__ __forceinline__ void eig_quad(const double* __restrict__ lam_pair, int q, int M, double C, T& fq, T& fnq,
+                                         T& fmq, T& fpq) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(lam_pair) + q);
+    const double2 b = __ldg(reinterpret_cast<const double2*>(lam_pair) + (M - q));
+    fq = (T)recip_f64(a.x + C);
+    fnq = (T)recip_f64(a.y + C);
+    fmq = (T)recip_f64(b.x + C);
+    fpq = (T)recip_f64(b.y + C);
+}
 // ... and 0 on the null mode (lam == 0)
 template <typename T>
 __device__ __forceinline__ T eig_recip(const double* __restrict__ lam_t, int kt, double C) {

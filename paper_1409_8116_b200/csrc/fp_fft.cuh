@@ -980,8 +980,9 @@ __device__ __forceinline__ void compute_store(const FftPass& p, const LineInfo* 
                 const double C = line_lam_sum(L);
                 auto quad = [&](int q) {
                     cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-                    mid_quad<T>(zk, zm, Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C), eig_recip_nz<T>(lt, KPHYS(n - q), C),
-                                eig_recip_nz<T>(lt, KPHYS(M - q), C), eig_recip_nz<T>(lt, KPHYS(M + q), C));
+                    T f0, f1, f2, f3;
+                    eig_quad<T>(Sc.lam_pair, q, M, C, f0, f1, f2, f3);
+                    mid_quad<T>(zk, zm, Ww[q], Wb[q], f0, f1, f2, f3);
                     line_f[P(q)] = zk;
                     line_f[P(M - q)] = zm;
                 };
@@ -1272,9 +1273,9 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
                             const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
                             half0 = rmerge<T>(Vh, Vh, th);
                         } else {
-                            mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C),
-                                        eig_recip_nz<T>(lt, KPHYS(n - q), C), eig_recip_nz<T>(lt, KPHYS(M - q), C),
-                                        eig_recip_nz<T>(lt, KPHYS(M + q), C));
+                            T f0, f1, f2, f3;
+                            eig_quad<T>(Sc.lam_pair, q, M, C, f0, f1, f2, f3);
+                            mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], f0, f1, f2, f3);
                         }
                     }
 #undef KPHYS

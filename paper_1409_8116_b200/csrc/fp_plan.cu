@@ -73,6 +73,7 @@ struct DevTables {
     void* wt = nullptr;
     void* ww = nullptr;
     void* wb = nullptr;     // folded DCT-II / DST-II MID twiddle (fp_tables.h mid_table)
+    void* lam2 = nullptr;   // folded MID eigenvalue pairs (Scaling::lam_pair)
     void* mat_f = nullptr;  // dense forward
     void* mat_b = nullptr;  // dense backward
     int fwd_nout = 0, fwd_nin = 0, bwd_nout = 0, bwd_nin = 0;
@@ -870,6 +871,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
     P->cpitch_last = (P->cext[d - 1] + 7) / 8 * 8;
     if (P->r_axis < 0 || P->cext[d - 1] == P->n[d - 1]) P->cpitch_last = P->cext[d - 1];
 
+    std::vector<double> lam_host[3];
     // eigenvalue tables (host mirror may pass numpy-built ones)
     for (int a = 0; a < d; ++a) {
         std::vector<double> lam;
@@ -877,6 +879,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         else lam = eigenvalue_table(AxisSpec{cfg->n[a], cfg->length[a], cfg->bc[a], cfg->kind[a]}, cfg->approx);
         // one leading pad entry: a DST-I axis on the FFT engine reads its table from
         // the pad (spectral index k = 1..M-1 <-> eigenvalue k - 1)
+        lam_host[a] = lam;
         lam.insert(lam.begin(), 0.0);
         void* dl = nullptr;
         if (cudaMalloc(&dl, lam.size() * sizeof(double)) != cudaSuccess) { delete P; return fail(FP_ERR_ALLOC, "cudaMalloc eigenvalue table"); }
@@ -907,6 +910,20 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
                 std::vector<long double> wb;
                 mid_table((int)cfg->n[a], Mx[a], wb);
                 if ((st = upload(P->allocs, wb, P->f32, &T.wb)) != FP_OK) { delete P; return st; }
+                // eigenvalue pairs at the physical indices of the quads (DST: k -> n-1-k)
+                const long long nn = cfg->n[a], MM = Mx[a];
+                const bool dst_ax = cfg->bc[a] == FP_BC_DIRICHLET;
+                auto kp = [&](long long k) { return dst_ax ? nn - 1 - k : k; };
+                std::vector<double> l2(2 * (size_t)(MM + 1), 0.0);
+                for (long long q = 0; q <= MM; ++q) {
+                    l2[2 * q] = lam_host[a][(size_t)kp(q)];
+                    l2[2 * q + 1] = q > 0 ? lam_host[a][(size_t)kp(nn - q)] : 0.0;
+                }
+                void* d2 = nullptr;
+                if (cudaMalloc(&d2, l2.size() * sizeof(double)) != cudaSuccess) { delete P; return fail(FP_ERR_ALLOC, "cudaMalloc eigenvalue pairs"); }
+                P->allocs.push_back(d2);
+                if (cudaMemcpy(d2, l2.data(), l2.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) { delete P; return fail(FP_ERR_CUDA, "upload eigenvalue pairs"); }
+                T.lam2 = d2;
             }
         } else {
             const int fk = cfg->bc[a] == FP_BC_PERIODIC ? (rf ? 100 : FP_DFT) : fwd[a];
@@ -988,6 +1005,7 @@ static fp_status build_plan(const fp_config* cfg, int device, int nranks, int ra
         Scaling& s = p.s;
         // DST-I spectra sit at k = 1..M-1 of the extended line: eigenvalue k - 1
         s.lam_t = (regular && dir) ? P->d_lam_pad[t] : P->d_lam[t];
+        s.lam_pair = (const double*)P->tab[t].lam2;
         s.lam_a = ps.a >= 0 ? P->d_lam[ps.a] : nullptr;
         s.lam_b = ps.b >= 0 ? P->d_lam[ps.b] : nullptr;
         s.pos_t = t; s.pos_a = ps.a; s.pos_b = ps.b;

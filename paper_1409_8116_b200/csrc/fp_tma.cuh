@@ -394,8 +394,9 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
         const double C = line_lam_sum(L);
         auto quad = [&](int q) {
             cx<T> zk = line_f[P(q)], zm = line_f[P(M - q)];
-            mid_quad<T>(zk, zm, Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C), eig_recip_nz<T>(lt, KPHYS(n - q), C),
-                        eig_recip_nz<T>(lt, KPHYS(M - q), C), eig_recip_nz<T>(lt, KPHYS(M + q), C));
+            T f0, f1, f2, f3;
+            eig_quad<T>(Sc.lam_pair, q, M, C, f0, f1, f2, f3);
+            mid_quad<T>(zk, zm, Ww[q], Wb[q], f0, f1, f2, f3);
             line_f[P(q)] = zk;
             line_f[P(M - q)] = zm;
         };
@@ -464,9 +465,9 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
                 const cx<T> Vh = cmulc<T>(mkc<T>(Xa, -Xb), wh);
                 half0 = rmerge<T>(Vh, Vh, th);
             } else {
-                mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], eig_recip_nz<T>(lt, KPHYS(q), C),
-                            eig_recip_nz<T>(lt, KPHYS(n - q), C), eig_recip_nz<T>(lt, KPHYS(M - q), C),
-                            eig_recip_nz<T>(lt, KPHYS(M + q), C));
+                T f0, f1, f2, f3;
+                eig_quad<T>(Sc.lam_pair, q, M, C, f0, f1, f2, f3);
+                mid_quad<T>(v[r], pz[r], Ww[q], Wb[q], f0, f1, f2, f3);
             }
         }
 #undef KPHYS

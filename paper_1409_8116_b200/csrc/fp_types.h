@@ -74,6 +74,9 @@ struct Scaling {
     double inv_np;              // 1 / prod n_periodic (solver.py:238-239)
     int singular;
     double* dc_out;             // raw null-mode coefficient sink (or nullptr)
+    // folded DCT-II / DST-II MID: (lam_t[KPHYS(q)], lam_t[KPHYS(n-q)]) for q = 0..M, fp64
+    // pairs, so one 16-B load serves a quad's (q, n-q) and another its (M-q, M+q)
+    const double* lam_pair;
 };
 
 // rhs producer of a 2D projection step (flow.py:114-122, 290): the first pass
