@@ -20,7 +20,7 @@ LIB_PATH = LIB_DIR / "libfastpoisson_b200.so"
 
 SOURCES = [f"fp_fft_{t}_l{g}.cu" for t in ("d", "f") for g in (4, 6, 8, 9, 11, 12)] + [
     "fp_kernels.cu", "fp_mr.cu", "fp_blue.cu", "fp_tma.cu", "fp_plan.cu", "fp_tables.cpp"]
-HEADERS = ["fp_types.h", "fp_tables.h", "fp_common.cuh", "fp_fft.cuh", "fp_tma.cuh"]
+HEADERS = ["fp_types.h", "fp_tables.h", "fp_common.cuh", "fp_fft.cuh", "fp_tma.cuh", "fp_attr.h"]
 OBJ_DIR = PKG / "build"
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]

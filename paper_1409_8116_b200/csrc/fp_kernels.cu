@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "fp_attr.h"
 #include "fp_common.cuh"
 
 namespace fpb {
@@ -467,9 +468,7 @@ static cudaError_t allow_smem(const void* fn) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
 }
 
-static cudaError_t set_smem_attr() {
-    static bool done = false;
-    if (done) return cudaSuccess;
+static cudaError_t set_smem_attr_all() {
     cudaError_t e;
     for (int l = 4; l <= 13; ++l)
         for (int s = 0; s < 2; ++s)
@@ -485,8 +484,12 @@ static cudaError_t set_smem_attr() {
             if ((e = allow_smem((const void*)pick_wide(l, true, op))) != cudaSuccess) return e;
     if ((e = allow_smem((const void*)dense_pass_kernel<double>)) != cudaSuccess) return e;
     if ((e = allow_smem((const void*)dense_pass_kernel<float>)) != cudaSuccess) return e;
-    done = true;
     return cudaSuccess;
+}
+// (once per device: the opt-in belongs to the device context)
+static cudaError_t set_smem_attr() {
+    static PerDeviceOnce once;
+    return once.run(set_smem_attr_all);
 }
 
 static int env_flag(const char* name, int dflt) {
@@ -554,13 +557,8 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
 
 template <typename T, int CLS, int LT>
 static cudaError_t launch_dense_tile_lt(const DensePass& p, size_t smem, long long tiles, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(dense_tile_kernel<T, CLS, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)dense_tile_kernel<T, CLS, LT>);
+    if (e != cudaSuccess) return e;
     dense_tile_kernel<T, CLS, LT><<<(unsigned)tiles, 256, smem, st>>>(p);
     return cudaGetLastError();
 }

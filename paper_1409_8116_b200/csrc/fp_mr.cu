@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/fastpoisson_b200.h"
+#include "fp_attr.h"
 #include "fp_common.cuh"
 
 namespace fpb {
@@ -672,13 +673,8 @@ cudaError_t launch_mr_pass(const MrPass& p, bool f32, cudaStream_t st) {
     if (p.g.in_type != (cin ? ct : rt) || p.g.out_type != (cout ? ct : rt)) return cudaErrorInvalidValue;
     MrKernelFn fn = f32 ? mr_pick<float>(p.kind, p.mid != 0, p.half != 0) : mr_pick<double>(p.kind, p.mid != 0, p.half != 0);
     if (!fn) return cudaErrorInvalidValue;
-    static bool attr[2][64] = {};
-    const int key = (p.half ? 32 : 0) + (p.mid ? 16 : 0) + (p.kind >= 100 ? 10 + p.kind - 100 : p.kind);
-    if (!attr[f32][key]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr[f32][key] = true;
-    }
+    cudaError_t e = ensure_smem_attr((const void*)fn);
+    if (e != cudaSuccess) return e;
     fn<<<p.tiles, 256, mr_smem_bytes(p, f32), st>>>(p);
     return cudaGetLastError();
 }

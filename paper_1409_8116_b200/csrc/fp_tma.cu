@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "fp_attr.h"
 #include "fp_tma.cuh"
 
 namespace fpb {
@@ -120,13 +121,8 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
     FftKernelFn fn = tma_kernel_for(p);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = tma_smem_bytes(p, (size_t)(2 * p.M) * 128);
-    static bool attr[2][3][2][2] = {};
-    bool& a = attr[p.logM - 7][p.op][p.fkind == FK_DST2][tma_mode(p.op) == 2];
-    if (!a) {
-        cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        a = true;
-    }
+    const cudaError_t e = ensure_smem_attr((const void*)fn);
+    if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);
     fn<<<p.tiles, threads, smem, st>>>(p);
     return cudaGetLastError();
