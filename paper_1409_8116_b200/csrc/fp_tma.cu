@@ -35,26 +35,30 @@ bool tma_enabled() {
     return on;
 }
 
-// 3D map over (columns b [stride 1], transform axis, a axis) of a real fp64 array;
-// dims 1 / 2 ordered by stride (tdim = the transform axis' dim).  `phase`: boxes of
-// 64 rows at traversal stride 4 (PHASE staging), else 256 consecutive rows.
-bool encode(CUtensorMap* map, const void* base, long long nb, long long nt, long long na, long long st,
-            long long sa, bool phase, int* tdim) {
+// 3D map over (columns b [stride 1], transform axis, a axis) of an fp64 array (complex:
+// two doubles per column); dims 1 / 2 ordered by stride (tdim = the transform axis' dim).
+// Box: `cols` doubles x `rows` rows traversed at `estride` (PHASE / PAIR staging: 4 / 2).
+bool encode(CUtensorMap* map, const void* base, long long ncols, long long nt, long long na, long long st_bytes,
+            long long sa_bytes, int cols, int rows, int estride, CUtensorMapSwizzle swz, int* tdim) {
     EncodeFn fn = encode_fn();
     if (!fn) return false;
-    const bool t_first = st <= sa || na <= 1;
-    cuuint64_t dims[3] = {(cuuint64_t)nb, (cuuint64_t)(t_first ? nt : na), (cuuint64_t)(t_first ? na : nt)};
-    cuuint64_t strides[2] = {(cuuint64_t)((t_first ? st : sa) * 8), (cuuint64_t)((t_first ? sa : st) * 8)};
+    const bool t_first = st_bytes <= sa_bytes || na <= 1;
+    cuuint64_t dims[3] = {(cuuint64_t)ncols, (cuuint64_t)(t_first ? nt : na), (cuuint64_t)(t_first ? na : nt)};
+    cuuint64_t strides[2] = {(cuuint64_t)(t_first ? st_bytes : sa_bytes), (cuuint64_t)(t_first ? sa_bytes : st_bytes)};
     if (na <= 1) strides[1] = strides[0] * (cuuint64_t)nt;   // (a dummy axis: any consistent stride)
-    cuuint32_t box[3] = {16, 1, 1};
+    cuuint32_t box[3] = {(cuuint32_t)cols, 1, 1};
     cuuint32_t es[3] = {1, 1, 1};
     const int td = t_first ? 1 : 2;
-    box[td] = 256;
-    es[td] = phase ? 4 : 1;
+    box[td] = (cuuint32_t)rows;
+    es[td] = (cuuint32_t)estride;
     *tdim = td;
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+bool encode_real(CUtensorMap* map, const void* base, long long nb, long long nt, long long na, long long st,
+                 long long sa, bool phase, int* tdim) {
+    return encode(map, base, nb, nt, na, st * 8, sa * 8, 16, 256, phase ? 4 : 1, CU_TENSOR_MAP_SWIZZLE_128B, tdim);
 }
 
 // per-op variant (FP_TMA_FWD / FP_TMA_INV / FP_TMA_MID): 0 = regular kernel, 1 = the
@@ -92,8 +96,39 @@ FftKernelFn tma_kernel_for(const FftPass& p) {
 // fp64 DCT-II / DST-II forward, DCT-III / DST-III inverse, or their MID, strided
 // over 16 adjacent columns (128-B rows) of plan-typed operands with 16-B aligned
 // rows, M = 128 or 256 (one 128-B row segment per line per tile)
+// real-FFT passes (c4's y axis): fp64, M = 512, 8 columns (64-B real rows, 128-B complex rows)
+static bool tma_prepare_rfft(FftPass& p) {
+    const Geometry& g = p.g;
+    const bool fwd = p.op == OP_FWD && p.fkind == FK_RFFT;
+    const bool inv = p.op == OP_INV && p.ikind == IK_IRFFT;
+    if (!(fwd || inv) || p.lines != 8 || p.logM != 9) return false;
+    if (g.blk_lg > 0 || g.row_tab || g.pair_b || g.a_lim > 0 || g.b_lim > 0 || p.prod.active) return false;
+    const int rt = fwd ? g.in_type : g.out_type, ct = fwd ? g.out_type : g.in_type;
+    if (rt != ET_F64 || ct != ET_C128) return false;
+    if ((g.nb > 1 && (g.in_sb != 1 || g.out_sb != 1)) || g.nb < 1) return false;
+    const long long rst = fwd ? g.in_st : g.out_st, rsa = fwd ? g.in_sa : g.out_sa;   // real operand (doubles)
+    const long long cst = fwd ? g.out_st : g.in_st, csa = fwd ? g.out_sa : g.in_sa;   // complex operand (complex)
+    if ((rst * 8) % 16 || (g.na > 1 && (rsa * 8) % 16)) return false;
+    if (((uintptr_t)g.in % 16) || ((uintptr_t)g.out % 16)) return false;
+    const void* rbase = fwd ? g.in : g.out;
+    const void* cbase = fwd ? g.out : g.in;
+    const long long M = p.M;
+    int td_r = 0, td_c = 0, td_a = 0;
+    CUtensorMap* rmap = fwd ? &p.tm_in : &p.tm_out;
+    CUtensorMap* cmap = fwd ? &p.tm_out : &p.tm_in;
+    if (!encode(rmap, rbase, g.nb, 2 * M, g.na, rst * 8, rsa * 8, 8, 256, 2, CU_TENSOR_MAP_SWIZZLE_64B, &td_r)) return false;
+    if (!encode(cmap, cbase, 2 * g.nb, M + 1, g.na, cst * 16, csa * 16, 16, 256, 1, CU_TENSOR_MAP_SWIZZLE_128B, &td_c)) return false;
+    if (!encode(&p.tm_aux, cbase, 2 * g.nb, M + 1, g.na, cst * 16, csa * 16, 16, 8, 1, CU_TENSOR_MAP_SWIZZLE_128B, &td_a)) return false;
+    if (td_r != td_c || td_c != td_a) return false;
+    p.tm_tdim = td_r;
+    p.tma = 2;
+    return true;
+}
+
 bool tma_prepare(FftPass& p, bool f32) {
     p.tma = 0;
+    static const bool rfft_on = env_mode("FP_TMA_RFFT", 1) != 0;
+    if (tma_enabled() && !f32 && p.family == FAM_STRIDED && rfft_on && tma_prepare_rfft(p)) return true;
     if (!tma_enabled() || f32 || p.family != FAM_STRIDED || p.lines != 16 || (p.logM != 7 && p.logM != 8)) return false;
     if (tma_mode(p.op) == 0) return false;
     const bool real_fwd = p.fkind == FK_DCT2 || p.fkind == FK_DST2;
@@ -109,8 +144,8 @@ bool tma_prepare(FftPass& p, bool f32) {
     const long long nreal = 2LL * p.M;
     int td_in = 0, td_out = 0;
     const bool phase_in = p.op != OP_INV, phase_out = p.op != OP_FWD;
-    if (!encode(&p.tm_in, g.in, g.nb, nreal, g.na, g.in_st, g.in_sa, phase_in, &td_in)) return false;
-    if (!encode(&p.tm_out, g.out, g.nb, nreal, g.na, g.out_st, g.out_sa, phase_out, &td_out)) return false;
+    if (!encode_real(&p.tm_in, g.in, g.nb, nreal, g.na, g.in_st, g.in_sa, phase_in, &td_in)) return false;
+    if (!encode_real(&p.tm_out, g.out, g.nb, nreal, g.na, g.out_st, g.out_sa, phase_out, &td_out)) return false;
     if (td_in != td_out) return false;
     p.tm_tdim = td_in;
     p.tma = 1;
@@ -118,6 +153,15 @@ bool tma_prepare(FftPass& p, bool f32) {
 }
 
 cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
+    if (p.tma == 2) {   // real-FFT lines
+        FftKernelFn fn = p.op == OP_FWD ? fft_pass_tma_r<9, OP_FWD> : fft_pass_tma_r<9, OP_INV>;
+        const size_t tile = (size_t)p.lines * p.ls * 16, cstg = (size_t)(p.M + 8) * 128;
+        const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > cstg ? tile : cstg) + 16;
+        const cudaError_t e = ensure_smem_attr((const void*)fn);
+        if (e != cudaSuccess) return e;
+        fn<<<p.tiles, p.lines << (p.logM - 4), smem, st>>>(p);
+        return cudaGetLastError();
+    }
     FftKernelFn fn = tma_kernel_for(p);
     if (!fn) return cudaErrorInvalidValue;
     const size_t smem = tma_smem_bytes(p, (size_t)(2 * p.M) * 128);

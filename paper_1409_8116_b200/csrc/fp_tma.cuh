@@ -481,4 +481,172 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
     }
 }
 
+// ----------------------------------------------------------------------------
+// Real-FFT lines (periodic axis transformed as a real FFT on a strided axis: c4's y
+// passes): n = 2M = 1024 real points, 8 adjacent columns (64-B rows), TL = 32.
+//   forward: real rows in PAIR staging -- rows y = 2t + phi in sub-tile phi, row t
+//            (traversal stride 2), so z_m = (x_2m, x_2m+1) is row m of both sub-tiles --
+//            -> FFT -> untangle -> complex half spectrum X_0..X_M in NATURAL rows of
+//            8 complex (128 B) -> TMA store;
+//   inverse: the half spectrum from NATURAL complex rows -> tangle -> inverse FFT ->
+//            the real pairs back into PAIR staging -> TMA store.
+// 64-B rows (SWIZZLE_64B): 16-B chunk c of row r at chunk c ^ ((r >> 1) & 3)
+__device__ __forceinline__ int stg_off64(int r, int byte) {
+    return r * 64 + (((((byte >> 4) ^ (r >> 1)) & 3)) << 4) + (byte & 15);
+}
+template <int N>   // PAIR sub-tile phi (n/2 rows of 64 B) starts at phi * (n/2) * 64
+__device__ __forceinline__ double& stg_pair(unsigned char* stg, int phi, int t, int c) {
+    return *reinterpret_cast<double*>(stg + phi * (N / 2) * 64 + stg_off64(t, c * 8));
+}
+__device__ __forceinline__ cx<double>& stg_cnat(unsigned char* stg, int r, int c) {   // 8 complex per row
+    return *reinterpret_cast<cx<double>*>(stg + r * 128 + (((c ^ r) & 7) << 4));
+}
+
+template <int LOGM, int OP>
+__global__ void __launch_bounds__(256, 2) fft_pass_tma_r(const __grid_constant__ FftPass p) {
+    using T = double;
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, n = 2 * M;
+    constexpr bool kFwd = opb(OP) == OP_FWD;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    unsigned char* const b0 = smem_raw + linfo_bytes(p.lines);
+    unsigned char* stg = b0 + ((1024u - (smem_addr(b0) & 1023u)) & 1023u);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(stg);
+    const size_t tile = (size_t)p.lines * p.ls * 16;
+    const size_t cstg = (size_t)(M + 8) * 128;
+    const size_t region = tile > cstg ? tile : cstg;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + region);
+    const int tid = threadIdx.x;
+    const TmaTile tt = tma_tile(p);
+    int c1, c2;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        if constexpr (kFwd) {   // PAIR staging: 2 phases x n/512 boxes of 128 rows (traversal stride 2)
+            mbar_expect_tx(bar, (unsigned)n * 64u);
+#pragma unroll
+            for (int phi = 0; phi < 2; ++phi)
+#pragma unroll
+                for (int h = 0; h < n / 256; ++h) {
+                    tma_coords(p, tt, phi + 256 * h, &c1, &c2);
+                    tma_load_3d(stg + (phi * (n / 2) + 128 * h) * 64, &p.tm_in, tt.c0, c1, c2, bar);
+                }
+        } else {                // NATURAL complex rows 0..M: boxes of 256 rows + one of 8 (tm_aux)
+            mbar_expect_tx(bar, (unsigned)(M + 8) * 128u);
+#pragma unroll
+            for (int h = 0; h < M / 256; ++h) {
+                tma_coords(p, tt, 256 * h, &c1, &c2);
+                tma_load_3d(stg + 256 * h * 128, &p.tm_in, 2 * tt.c0, c1, c2, bar);
+            }
+            tma_coords(p, tt, M, &c1, &c2);
+            tma_load_3d(stg + M * 128, &p.tm_aux, 2 * tt.c0, c1, c2, bar);
+        }
+    }
+    setup_lines<true, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+    const int lf = tid >> LOGTL, jt = tid & (TL - 1);
+    const int lane = tid & 31;
+    const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
+    const int LS = line_stride<T, LOGM, true>(p);
+    cx<T>* line_f = sm + lf * LS;
+    const void* __restrict__ W = p.wfft;
+    const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
+    const LineInfo L = linfo[lf];
+    const T om = (T)p.out_mult;
+    cx<T> v[16], pz[8];
+    mbar_wait(bar, 0);
+    if constexpr (kFwd) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int m = jt + TL * s;
+            v[s] = mkc<T>(stg_pair<n>(stg, 0, m, lf), stg_pair<n>(stg, 1, m, lf));
+        }
+        if (p.nonfinite && L.valid) {
+            bool bad = false;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) bad |= !(finite_t(v[s].x) && finite_t(v[s].y));
+            if (bad) *p.nonfinite = 1;
+        }
+        fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        fetch_mirror<T>(v, pz, jt, partner);
+        __syncthreads();   // the complex staging overwrites the tile
+        const T omh = om * (T)0.5;
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq_unused;
+            qt.get(q, tq, wq_unused);
+            if (r == 0 && jt == 0) {
+                const cx<T> z0 = v[0], zh = v[8];
+                stg_cnat(stg, 0, lf) = mkc<T>((z0.x + z0.y) * om, 0);
+                stg_cnat(stg, M, lf) = mkc<T>((z0.x - z0.y) * om, 0);
+                stg_cnat(stg, HALF, lf) = cscale<T>(rsplit2<T>(zh, zh, Wt[HALF]), omh);
+            } else {
+                stg_cnat(stg, q, lf) = cscale<T>(rsplit2<T>(v[r], pz[r], tq), omh);
+                stg_cnat(stg, M - q, lf) = cscale<T>(rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)), omh);
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int h = 0; h < M / 256; ++h) {
+                tma_coords(p, tt, 256 * h, &c1, &c2);
+                tma_store_3d(&p.tm_out, 2 * tt.c0, c1, c2, stg + 256 * h * 128);
+            }
+            tma_coords(p, tt, M, &c1, &c2);   // row M (the 8-row box is clipped to the tensor)
+            tma_store_3d(&p.tm_aux, 2 * tt.c0, c1, c2, stg + M * 128);
+            tma_store_commit_wait();
+        }
+    } else {
+        cx<T> half0 = mkc<T>(0, 0);
+        if (p.nonfinite && L.valid) {
+            bool bad = false;
+            for (int k = jt; k <= M; k += TL) {
+                const cx<T> x = stg_cnat(stg, k, lf);
+                bad |= !(finite_t(x.x) && finite_t(x.y));
+            }
+            if (bad) *p.nonfinite = 1;
+        }
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, nullptr, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq_unused;
+            qt.get(q, tq, wq_unused);
+            if (r == 0 && jt == 0) {
+                const cx<T> x0 = stg_cnat(stg, 0, lf), xM = stg_cnat(stg, M, lf), xh = stg_cnat(stg, HALF, lf);
+                v[0] = rmerge<T>(x0, xM, mkc<T>(1, 0));
+                half0 = rmerge<T>(xh, xh, Wt[HALF]);
+            } else {
+                const cx<T> xk = stg_cnat(stg, q, lf), xm = stg_cnat(stg, M - q, lf);
+                v[r] = rmerge<T>(xk, xm, tq);
+                pz[r] = rmerge<T>(xm, xk, t_mirror<T>(tq));
+            }
+        }
+        return_mirror<T>(v, pz, jt, partner, half0);
+        fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int m = jt + TL * s;
+            stg_pair<n>(stg, 0, m, lf) = v[s].x * om;
+            stg_pair<n>(stg, 1, m, lf) = v[s].y * om;
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int phi = 0; phi < 2; ++phi)
+#pragma unroll
+                for (int h = 0; h < n / 256; ++h) {
+                    tma_coords(p, tt, phi + 256 * h, &c1, &c2);
+                    tma_store_3d(&p.tm_out, tt.c0, c1, c2, stg + (phi * (n / 2) + 128 * h) * 64);
+                }
+            tma_store_commit_wait();
+        }
+    }
+}
+
 }  // namespace fpb

@@ -116,6 +116,7 @@ struct FftPass {
     // solve time by tma_prepare; tm_tdim = the map dimension of the transform axis
     int tma, tm_tdim;
     CUtensorMap tm_in, tm_out;
+    CUtensorMap tm_aux;         // real-FFT passes: 8-row boxes of the complex half spectrum (row M)
 };
 
 struct DensePass {

@@ -24,6 +24,10 @@ CASES = {
     "wall_first_pass": orc.Case([(512, 1.0, N_, S_), (48, orc.TWO_PI, P_), (32, orc.TWO_PI, P_)], orc.SPECTRAL),
     "c3_quarter": orc.Case([(128, 1.0, N_, S_), (256, 1.0, N_, S_), (512, 1.0, N_, S_)], orc.FD2),
     "dst_c3_like": orc.Case([(256, 1.0, D_, S_), (512, 1.0, D_, S_), (64, 1.0, D_, S_)], orc.SPECTRAL),
+    # c4's pattern: the real-FFT axis (1024 points) strided between the wall axis and the MID:
+    # the real-FFT forward / inverse on the TMA kernel (8-column tiles, ragged: 36 columns)
+    "rfft_c4_like": orc.Case([(16, orc.TWO_PI, P_), (1024, orc.TWO_PI, P_), (36, 2.0, N_, S_)], orc.FD2),
+    "rfft_dir": orc.Case([(8, 1.0, P_), (1024, 2.0, P_), (64, 1.0, D_, S_)], orc.SPECTRAL),
 }
 
 
