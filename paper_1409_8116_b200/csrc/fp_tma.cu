@@ -125,8 +125,27 @@ static bool tma_prepare_rfft(FftPass& p) {
     return true;
 }
 
+// complex-line MID (c4's x axis): fp64, M = 1024, 4 columns (64-B rows)
+static bool tma_prepare_cmid(FftPass& p) {
+    const Geometry& g = p.g;
+    if (p.op != OP_MID || p.fkind != FK_CFFT || p.lines != 4 || p.logM != 10 || p.sub == 2) return false;
+    if (g.blk_lg > 0 || g.row_tab || g.pair_b || g.a_lim > 0 || g.b_lim > 0 || p.prod.active) return false;
+    if (g.in_type != ET_C128 || g.out_type != ET_C128) return false;
+    if ((g.nb > 1 && (g.in_sb != 1 || g.out_sb != 1)) || g.nb < 1) return false;
+    if (((uintptr_t)g.in % 16) || ((uintptr_t)g.out % 16)) return false;
+    int td_i = 0, td_o = 0;
+    if (!encode(&p.tm_in, g.in, 2 * g.nb, p.M, g.na, g.in_st * 16, g.in_sa * 16, 8, 256, 1, CU_TENSOR_MAP_SWIZZLE_64B, &td_i)) return false;
+    if (!encode(&p.tm_out, g.out, 2 * g.nb, p.M, g.na, g.out_st * 16, g.out_sa * 16, 8, 256, 1, CU_TENSOR_MAP_SWIZZLE_64B, &td_o)) return false;
+    if (td_i != td_o) return false;
+    p.tm_tdim = td_i;
+    p.tma = 3;
+    return true;
+}
+
 bool tma_prepare(FftPass& p, bool f32) {
     p.tma = 0;
+    static const bool cmid_on = env_mode("FP_TMA_CMID", 1) != 0;
+    if (tma_enabled() && !f32 && p.family == FAM_STRIDED && cmid_on && tma_prepare_cmid(p)) return true;
     static const bool rfft_on = env_mode("FP_TMA_RFFT", 1) != 0;
     if (tma_enabled() && !f32 && p.family == FAM_STRIDED && rfft_on && tma_prepare_rfft(p)) return true;
     if (!tma_enabled() || f32 || p.family != FAM_STRIDED || p.lines != 16 || (p.logM != 7 && p.logM != 8)) return false;
@@ -153,6 +172,15 @@ bool tma_prepare(FftPass& p, bool f32) {
 }
 
 cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
+    if (p.tma == 3) {   // complex-line MID
+        FftKernelFn fn = fft_pass_tma_c<10>;
+        const size_t tile = (size_t)p.lines * p.ls * 16, cstg = (size_t)p.M * 64;
+        const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > cstg ? tile : cstg) + 16;
+        const cudaError_t e = ensure_smem_attr((const void*)fn);
+        if (e != cudaSuccess) return e;
+        fn<<<p.tiles, p.lines << (p.logM - 4), smem, st>>>(p);
+        return cudaGetLastError();
+    }
     if (p.tma == 2) {   // real-FFT lines
         FftKernelFn fn = p.op == OP_FWD ? fft_pass_tma_r<9, OP_FWD> : fft_pass_tma_r<9, OP_INV>;
         const size_t tile = (size_t)p.lines * p.ls * 16, cstg = (size_t)(p.M + 8) * 128;

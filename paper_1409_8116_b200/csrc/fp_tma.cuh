@@ -649,4 +649,86 @@ __global__ void __launch_bounds__(256, 2) fft_pass_tma_r(const __grid_constant__
     }
 }
 
+// ----------------------------------------------------------------------------
+// Complex lines (the MID over a complex state: c4's x axis after the real FFT along y):
+// M = 1024 complex fp64 points, 4 adjacent columns (64-B rows of 4 complex), TL = 64.
+// NATURAL staging (row k = z_k; SWIZZLE_64B: eight consecutive rows of one column fall
+// in eight distinct 16-B bank groups); the first forward stage reads its butterfly
+// inputs from the staged rows, the eigenvalue divide is pointwise on the registers the
+// last forward stage leaves, and the last inverse stage's outputs go back to the rows.
+__device__ __forceinline__ cx<double>& stg_c64(unsigned char* stg, int r, int c) {   // 4 complex per row
+    return *reinterpret_cast<cx<double>*>(stg + stg_off64(r, c * 16));
+}
+
+template <int LOGM>
+__global__ void __launch_bounds__(256, 2) fft_pass_tma_c(const __grid_constant__ FftPass p) {
+    using T = double;
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
+    constexpr int OP = mid_op(FK_CFFT);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    unsigned char* const b0 = smem_raw + linfo_bytes(p.lines);
+    unsigned char* stg = b0 + ((1024u - (smem_addr(b0) & 1023u)) & 1023u);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(stg);
+    const size_t tile = (size_t)p.lines * p.ls * 16, cstg = (size_t)M * 64;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + (tile > cstg ? tile : cstg));
+    const int tid = threadIdx.x;
+    const TmaTile tt = tma_tile(p);
+    int c1, c2;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, (unsigned)M * 64u);
+#pragma unroll
+        for (int h = 0; h < M / 256; ++h) {
+            tma_coords(p, tt, 256 * h, &c1, &c2);
+            tma_load_3d(stg + 256 * h * 64, &p.tm_in, 2 * tt.c0, c1, c2, bar);
+        }
+    }
+    setup_lines<true, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+    const int lf = tid >> LOGTL, jt = tid & (TL - 1);
+    const int LS = line_stride<T, LOGM, true>(p);
+    cx<T>* line_f = sm + lf * LS;
+    const void* __restrict__ W = p.wfft;
+    const LineInfo L = linfo[lf];
+    cx<T> v[16];
+    mbar_wait(bar, 0);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = stg_c64(stg, jt + TL * s, lf);
+    if (p.nonfinite && L.valid) {
+        bool bad = false;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) bad |= !(finite_t(v[s].x) && finite_t(v[s].y));
+        if (bad) *p.nonfinite = 1;
+    }
+    fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+    const Scaling& Sc = p.s;
+    const bool cap = Sc.singular && Sc.dc_out && L.null_line && L.valid;
+    const double cst = Sc.bscale * Sc.inv_np;
+    if (jt == 0) {
+        if (cap) *Sc.dc_out = (double)v[0].x;
+        v[0] = cscale<T>(v[0], eig_factor<T>(Sc, L, 0));
+    } else {
+        v[0] = cscale<T>(v[0], eig_factor_nz<T>(Sc, L, jt, cst));
+    }
+#pragma unroll
+    for (int it = 1; it < 16; ++it) v[it] = cscale<T>(v[it], eig_factor_nz<T>(Sc, L, jt + it * TL, cst));
+    fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+    __syncthreads();
+    const T om = (T)p.out_mult;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) stg_c64(stg, jt + TL * s, lf) = cscale<T>(v[s], om);
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+        for (int h = 0; h < M / 256; ++h) {
+            tma_coords(p, tt, 256 * h, &c1, &c2);
+            tma_store_3d(&p.tm_out, 2 * tt.c0, c1, c2, stg + 256 * h * 64);
+        }
+        tma_store_commit_wait();
+    }
+}
+
 }  // namespace fpb

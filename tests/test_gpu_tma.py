@@ -28,6 +28,9 @@ CASES = {
     # the real-FFT forward / inverse on the TMA kernel (8-column tiles, ragged: 36 columns)
     "rfft_c4_like": orc.Case([(16, orc.TWO_PI, P_), (1024, orc.TWO_PI, P_), (36, 2.0, N_, S_)], orc.FD2),
     "rfft_dir": orc.Case([(8, 1.0, P_), (1024, 2.0, P_), (64, 1.0, D_, S_)], orc.SPECTRAL),
+    # the MID over a complex state (c4's x axis): 1024-point complex lines, 4-column tiles (ragged: 22)
+    "cmid_c4_like": orc.Case([(1024, orc.TWO_PI, P_), (16, orc.TWO_PI, P_), (22, 2.0, N_, S_)], orc.FD2),
+    "cmid_spectral": orc.Case([(1024, orc.TWO_PI, P_), (10, orc.TWO_PI, P_), (32, 1.0, D_, S_)], orc.SPECTRAL),
 }
 
 
