@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <mutex>
 #include <set>
 #include <utility>
@@ -45,5 +47,28 @@ class PerDeviceOnce {
     std::mutex mu_;
     unsigned long long mask_ = 0;
 };
+
+// Programmatic dependent launch (FP_PDL, default on): an FFT pass launched with
+// programmatic stream serialization is scheduled while its predecessor drains and waits
+// on the device (griddepcontrol.wait, first thing in every pass kernel) -- the launch
+// gap between the passes of a solve disappears (small, launch-bound grids: c1).
+inline bool pdl_enabled() {
+    static const bool on = [] { const char* v = std::getenv("FP_PDL"); return !(v && *v == '0'); }();
+    return on;
+}
+template <typename P>
+inline cudaError_t launch_pass(void (*fn)(P), dim3 grid, dim3 block, size_t smem, cudaStream_t st, const P& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, p);
+}
 
 }  // namespace fpb

@@ -8,6 +8,10 @@
 
 namespace fpb {
 
+// every pass kernel starts here: when launched as a programmatic dependent (fp_attr.h
+// launch_pass) it may be resident before the previous pass has finished -- wait for it
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ----------------------------------------------------------------------------
 // complex helpers
 template <typename T> struct CxOf;

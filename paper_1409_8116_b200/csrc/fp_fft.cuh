@@ -1342,6 +1342,7 @@ __device__ __forceinline__ void compute_store_reg(const FftPass& p, const LineIn
 // general path: one tile per CTA, loads straight from HBM
 template <typename T, int LOGM, bool STRIDED, int OP>
 __device__ __forceinline__ void fft_pass_tile(const FftPass& p) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using S = Shape<LOGM>;
     LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
@@ -1380,6 +1381,7 @@ __global__ void __launch_bounds__(512) fft_pass_kernel(const FftPass p) {
 // it from 50 to 97 ms, 64-B rows from 50 to 40 ms.)
 template <typename T, int LOGM, int OP>
 __global__ void __launch_bounds__(512) fft_pass_wide(const FftPass p) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using S = Shape<LOGM>;
     constexpr int TL = S::TL, LOGTL = S::LOGTL;
@@ -1539,6 +1541,7 @@ __device__ __forceinline__ void issue_tile_async(const FftPass& p, const LineInf
 
 template <typename T, int LOGM, int OP>
 __global__ void __launch_bounds__(512) fft_pass_spipe(const FftPass p) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     using S = Shape<LOGM>;
     const unsigned lib = (unsigned)linfo_bytes(p.lines);

@@ -535,24 +535,21 @@ cudaError_t launch_fft_pass(const FftPass& p, bool f32, cudaStream_t st) {
             per_sm > 0) {
             long long grid = (long long)sms * per_sm;
             if (grid > p.tiles) grid = p.tiles;
-            fn<<<(int)grid, threads, psmem, st>>>(p);
-            return cudaGetLastError();
+            return launch_pass(fn, dim3((unsigned)grid), dim3(threads), psmem, st, p);
         }
     }
     const size_t smem = fft_pass_smem_bytes(p, rb);
     if (p.sub == 2) {
         FftKernelFn w = pick_wide(p.logM, f32, p.op);
         if (!w || !strided) return cudaErrorInvalidValue;
-        w<<<p.tiles, threads / 2, smem, st>>>(p);
-        return cudaGetLastError();
+        return launch_pass(w, dim3(p.tiles), dim3(threads / 2), smem, st, p);
     }
     static const int mid_spec = env_flag("FP_MID_KIND_KERNELS", 1);   // 0: one MID kernel for all kinds (A/B)
     const int kind = (p.op == OP_MID && mid_spec) ? p.fkind : -1;
     FftKernelFn fn = f32 ? pick_fft<float>(p.logM, strided, p.op, false, kind)
                          : pick_fft<double>(p.logM, strided, p.op, false, kind);
     if (!fn) return cudaErrorInvalidValue;
-    fn<<<p.tiles, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pass(fn, dim3(p.tiles), dim3(threads), smem, st, p);
 }
 
 template <typename T, int CLS, int LT>

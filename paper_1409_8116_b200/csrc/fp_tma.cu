@@ -178,8 +178,7 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
         const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > cstg ? tile : cstg) + 16;
         const cudaError_t e = ensure_smem_attr((const void*)fn);
         if (e != cudaSuccess) return e;
-        fn<<<p.tiles, p.lines << (p.logM - 4), smem, st>>>(p);
-        return cudaGetLastError();
+        return launch_pass(fn, dim3(p.tiles), dim3(p.lines << (p.logM - 4)), smem, st, p);
     }
     if (p.tma == 2) {   // real-FFT lines
         FftKernelFn fn = p.op == OP_FWD ? fft_pass_tma_r<9, OP_FWD> : fft_pass_tma_r<9, OP_INV>;
@@ -187,8 +186,7 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
         const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > cstg ? tile : cstg) + 16;
         const cudaError_t e = ensure_smem_attr((const void*)fn);
         if (e != cudaSuccess) return e;
-        fn<<<p.tiles, p.lines << (p.logM - 4), smem, st>>>(p);
-        return cudaGetLastError();
+        return launch_pass(fn, dim3(p.tiles), dim3(p.lines << (p.logM - 4)), smem, st, p);
     }
     FftKernelFn fn = tma_kernel_for(p);
     if (!fn) return cudaErrorInvalidValue;
@@ -196,8 +194,7 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
     const cudaError_t e = ensure_smem_attr((const void*)fn);
     if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);
-    fn<<<p.tiles, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    return launch_pass(fn, dim3(p.tiles), dim3(threads), smem, st, p);
 }
 
 }  // namespace fpb

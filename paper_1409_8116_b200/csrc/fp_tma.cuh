@@ -213,6 +213,7 @@ __host__ __device__ inline size_t tma_smem_bytes(const FftPass& p, size_t stage)
 // measured slower than their register paths, profiles/r02/ab_tma_variants.txt)
 template <int LOGM, int OP, bool SMEM = false>
 __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_constant__ FftPass p) {
+    pdl_wait();
     using T = double;
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, n = 2 * M;
@@ -504,6 +505,7 @@ __device__ __forceinline__ cx<double>& stg_cnat(unsigned char* stg, int r, int c
 
 template <int LOGM, int OP>
 __global__ void __launch_bounds__(256, 2) fft_pass_tma_r(const __grid_constant__ FftPass p) {
+    pdl_wait();
     using T = double;
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, n = 2 * M;
@@ -662,6 +664,7 @@ __device__ __forceinline__ cx<double>& stg_c64(unsigned char* stg, int r, int c)
 
 template <int LOGM>
 __global__ void __launch_bounds__(256, 2) fft_pass_tma_c(const __grid_constant__ FftPass p) {
+    pdl_wait();
     using T = double;
     using S = Shape<LOGM>;
     constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL;
