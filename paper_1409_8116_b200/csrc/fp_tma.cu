@@ -142,8 +142,41 @@ static bool tma_prepare_cmid(FftPass& p) {
     return true;
 }
 
+// contiguous DCT / DST lines (c3's z passes): fp64, n = 512, 2 lines per CTA
+static bool encode_lines(CUtensorMap* map, const void* base, long long n, long long nb, long long na, long long sb,
+                         long long sa, int lines) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {16, (cuuint64_t)(n / 16), (cuuint64_t)nb, (cuuint64_t)(na < 1 ? 1 : na)};
+    cuuint64_t strides[3] = {128, (cuuint64_t)(sb * 8), (cuuint64_t)(na > 1 ? sa * 8 : sb * 8 * nb)};
+    cuuint32_t box[4] = {16, (cuuint32_t)(n / 16), (cuuint32_t)lines, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool tma_prepare_z(FftPass& p) {
+    const Geometry& g = p.g;
+    const bool fwd = p.op == OP_FWD && (p.fkind == FK_DCT2 || p.fkind == FK_DST2);
+    const bool inv = p.op == OP_INV && (p.ikind == IK_DCT3 || p.ikind == IK_DST3);
+    if (!(fwd || inv) || p.logM != 8 || p.lines != 2 || p.family != FAM_CONTIG) return false;
+    if (g.blk_lg > 0 || g.row_tab || g.pair_b || g.a_lim > 0 || g.b_lim > 0 || p.prod.active) return false;
+    if (g.in_type != ET_F64 || g.out_type != ET_F64 || g.in_st != 1 || g.out_st != 1) return false;
+    if (g.nb % p.lines) return false;
+    auto ok16 = [](long long s) { return (s * 8) % 16 == 0; };
+    if ((g.nb > 1 && (!ok16(g.in_sb) || !ok16(g.out_sb))) || (g.na > 1 && (!ok16(g.in_sa) || !ok16(g.out_sa)))) return false;
+    if (((uintptr_t)g.in % 16) || ((uintptr_t)g.out % 16)) return false;
+    const long long n = 2LL * p.M;
+    if (!encode_lines(&p.tm_in, g.in, n, g.nb, g.na, g.in_sb, g.in_sa, p.lines)) return false;
+    if (!encode_lines(&p.tm_out, g.out, n, g.nb, g.na, g.out_sb, g.out_sa, p.lines)) return false;
+    p.tma = 5;
+    return true;
+}
+
 bool tma_prepare(FftPass& p, bool f32) {
     p.tma = 0;
+    static const bool z_on = env_mode("FP_TMA_Z", 1) != 0;
+    if (tma_enabled() && !f32 && z_on && tma_prepare_z(p)) return true;
     static const bool cmid_on = env_mode("FP_TMA_CMID", 1) != 0;
     if (tma_enabled() && !f32 && p.family == FAM_STRIDED && cmid_on && tma_prepare_cmid(p)) return true;
     static const bool rfft_on = env_mode("FP_TMA_RFFT", 1) != 0;
@@ -172,6 +205,14 @@ bool tma_prepare(FftPass& p, bool f32) {
 }
 
 cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
+    if (p.tma == 5) {   // contiguous DCT / DST lines
+        FftKernelFn fn = p.op == OP_FWD ? fft_pass_tma_z<8, OP_FWD> : fft_pass_tma_z<8, OP_INV>;
+        const size_t tile = (size_t)p.lines * Shape<8>::LS * 16, sb = (size_t)p.lines * 2 * p.M * 8;
+        const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > sb ? tile : sb) + 16;
+        const cudaError_t e = ensure_smem_attr((const void*)fn);
+        if (e != cudaSuccess) return e;
+        return launch_pass(fn, dim3(p.tiles), dim3(p.lines << (p.logM - 4)), smem, st, p);
+    }
     if (p.tma == 3) {   // complex-line MID
         FftKernelFn fn = fft_pass_tma_c<10>;
         const size_t tile = (size_t)p.lines * p.ls * 16, cstg = (size_t)p.M * 64;

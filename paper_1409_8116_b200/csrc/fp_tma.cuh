@@ -734,4 +734,157 @@ __global__ void __launch_bounds__(256, 2) fft_pass_tma_c(const __grid_constant__
     }
 }
 
+// ----------------------------------------------------------------------------
+// Contiguous DCT / DST lines (c3's z passes): L = 2 lines of n = 2M = 512 fp64 per CTA.
+// A 4D tensor map views each line as n/16 rows of 128 B; the CTA's box lands as
+// [line][row][16 doubles] with SWIZZLE_128B.  Forward: the Makhoul pairs (x_4m, x_4m+2)
+// / (x_2n-1-4m, x_2n-3-4m) straight into the first FFT stage, the DCT-II quads back as
+// natural rows; inverse: the DCT-III spectrum read in natural order, the de-Makhoul'd
+// output written back.  Element k of line l at l*n*8 + (k/16)*128 + swizzled chunk.
+template <int N>
+__device__ __forceinline__ double& stg_lin(unsigned char* stg, int l, int k) {
+    const int r = k >> 4, c = k & 15;
+    return *reinterpret_cast<double*>(stg + l * (N * 8) + r * 128 + ((((c >> 1) ^ r) & 7) << 4) + ((c & 1) << 3));
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                 ::"r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src)) : "memory");
+}
+
+template <int LOGM, int OP>   // OP_FWD (DCT-II / DST-II) or OP_INV (DCT-III / DST-III)
+__global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass p) {
+    pdl_wait();
+    using T = double;
+    using S = Shape<LOGM>;
+    constexpr int M = S::M, LOGTL = S::LOGTL, TL = S::TL, HALF = S::HALF, n = 2 * M;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LineInfo* linfo = reinterpret_cast<LineInfo*>(smem_raw);
+    unsigned char* const b0 = smem_raw + linfo_bytes(p.lines);
+    unsigned char* stg = b0 + ((1024u - (smem_addr(b0) & 1023u)) & 1023u);
+    cx<T>* sm = reinterpret_cast<cx<T>*>(stg);
+    const size_t tile = (size_t)p.lines * S::LS * 16, sbytes = (size_t)p.lines * n * 8;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + (tile > sbytes ? tile : sbytes));
+    const int tid = threadIdx.x;
+    const long long l0 = (long long)blockIdx.x * p.lines;
+    const int ia = (int)(l0 / p.g.nb), ib0 = (int)(l0 % p.g.nb);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        mbar_expect_tx(bar, (unsigned)sbytes);
+        tma_load_4d(stg, &p.tm_in, 0, 0, ib0, ia, bar);
+    }
+    setup_lines<false, OP>(p, blockIdx.x, linfo);
+    __syncthreads();
+    const int lf = tid >> LOGTL, jt = tid & (TL - 1);
+    const int lane = tid & 31;
+    const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
+    cx<T>* line_f = sm + lf * S::LS;
+    const void* __restrict__ W = p.wfft;
+    const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
+    const cx<T>* __restrict__ Ww = reinterpret_cast<const cx<T>*>(p.ww);
+    const LineInfo L = linfo[lf];
+    const T om = (T)p.out_mult;
+    cx<T> v[16], pz[8];
+    mbar_wait(bar, 0);
+    if (p.nonfinite && L.valid) {
+        bool bad = false;
+#pragma unroll
+        for (int i = 0; i < n / TL; ++i) bad |= !finite_t(stg_lin<n>(stg, lf, jt + TL * i));
+        if (bad) *p.nonfinite = 1;
+    }
+    if constexpr (opb(OP) == OP_FWD) {
+        const bool dst = p.fkind == FK_DST2;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int m = jt + TL * s;
+            double a, b;
+            if (s < 8) { a = stg_lin<n>(stg, lf, 4 * m); b = stg_lin<n>(stg, lf, 4 * m + 2); }
+            else {
+                a = stg_lin<n>(stg, lf, 2 * n - 1 - 4 * m);
+                b = stg_lin<n>(stg, lf, 2 * n - 3 - 4 * m);
+                if (dst) { a = -a; b = -b; }
+            }
+            v[s] = mkc<T>(a, b);
+        }
+        fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        fetch_mirror<T>(v, pz, jt, partner);
+        __syncthreads();
+        auto row = [&](int k) { return dst ? n - 1 - k : k; };
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq;
+            qt.get(q, tq, wq);
+            if (r == 0 && jt == 0) {
+                const cx<T> z0 = v[0], zh = v[8];
+                const cx<T> wM = Ww[M];
+                stg_lin<n>(stg, lf, row(0)) = (T)2 * (z0.x + z0.y) * om;
+                stg_lin<n>(stg, lf, row(M)) = (T)2 * (z0.x - z0.y) * wM.x * om;
+                const cx<T> U = cmul<T>(Ww[HALF], rsplit2<T>(zh, zh, Wt[HALF]));
+                stg_lin<n>(stg, lf, row(HALF)) = U.x * om;
+                stg_lin<n>(stg, lf, row(n - HALF)) = -U.y * om;
+            } else {
+                const cx<T> U1 = cmul<T>(wq, rsplit2<T>(v[r], pz[r], tq));
+                const cx<T> U2 = cmul<T>(w_mirror<T>(wq), rsplit2<T>(pz[r], v[r], t_mirror<T>(tq)));
+                stg_lin<n>(stg, lf, row(q)) = U1.x * om;
+                stg_lin<n>(stg, lf, row(n - q)) = -U1.y * om;
+                stg_lin<n>(stg, lf, row(M - q)) = U2.x * om;
+                stg_lin<n>(stg, lf, row(M + q)) = -U2.y * om;
+            }
+        }
+    } else {
+        const bool dst = p.ikind == IK_DST3;
+        auto X = [&](int k) { return stg_lin<n>(stg, lf, dst ? n - 1 - k : k); };
+        cx<T> half0 = mkc<T>(0, 0);
+        QuadTw<T, kTwPowQ<T, OP>> qt(Wt, Ww, jt, TL);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int q = jt + r * TL;
+            cx<T> tq, wq;
+            qt.get(q, tq, wq);
+            if (r == 0 && jt == 0) {
+                const T X0 = X(0), XM = X(M), Xh = X(HALF), Xnh = X(n - HALF);
+                const cx<T> wM = Ww[M];
+                const cx<T> VM = cmulc<T>(mkc<T>(XM, -XM), wM);
+                v[0] = rmerge<T>(mkc<T>(X0, 0), VM, mkc<T>(1, 0));
+                const cx<T> wh = Ww[HALF], th = Wt[HALF];
+                const cx<T> Vh = cmulc<T>(mkc<T>(Xh, -Xnh), wh);
+                half0 = rmerge<T>(Vh, Vh, th);
+            } else {
+                const T a = X(q), b = X(n - q), c = X(M - q), d = X(M + q);
+                const cx<T> wm = w_mirror<T>(wq), tm = t_mirror<T>(tq);
+                const cx<T> Vk = cmulc<T>(mkc<T>(a, -b), wq);
+                const cx<T> Vm = cmulc<T>(mkc<T>(c, -d), wm);
+                v[r] = rmerge<T>(Vk, Vm, tq);
+                pz[r] = rmerge<T>(Vm, Vk, tm);
+            }
+        }
+        return_mirror<T>(v, pz, jt, partner, half0);
+        fft_tile_reg_reg<true, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
+        __syncthreads();
+        const double oo = dst ? -om : om;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int m = jt + TL * s;
+            if (s < 8) {
+                stg_lin<n>(stg, lf, 4 * m) = v[s].x * om;
+                stg_lin<n>(stg, lf, 4 * m + 2) = v[s].y * om;
+            } else {
+                stg_lin<n>(stg, lf, 2 * n - 1 - 4 * m) = v[s].x * oo;
+                stg_lin<n>(stg, lf, 2 * n - 3 - 4 * m) = v[s].y * oo;
+            }
+        }
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        tma_store_4d(&p.tm_out, 0, 0, ib0, ia, stg);
+        tma_store_commit_wait();
+    }
+}
+
 }  // namespace fpb

@@ -29,6 +29,10 @@ CASES = {
     "rfft_c4_like": orc.Case([(16, orc.TWO_PI, P_), (1024, orc.TWO_PI, P_), (36, 2.0, N_, S_)], orc.FD2),
     "rfft_dir": orc.Case([(8, 1.0, P_), (1024, 2.0, P_), (64, 1.0, D_, S_)], orc.SPECTRAL),
     # the MID over a complex state (c4's x axis): 1024-point complex lines, 4-column tiles (ragged: 22)
+    # contiguous 512-point DCT / DST lines (c3's z passes) on the 4D-map kernel; odd line count: fallback
+    "z512_dst": orc.Case([(6, 1.0, D_, S_), (10, 1.0, D_, S_), (512, 1.0, D_, S_)], orc.FD2),
+    "z512_neu_2d": orc.Case([(30, 1.0, N_, S_), (512, 2.0, N_, S_)], orc.SPECTRAL),
+    "z512_odd_nb": orc.Case([(4, 1.0, N_, S_), (7, 1.0, N_, S_), (512, 1.0, N_, S_)], orc.FD2),
     "cmid_c4_like": orc.Case([(1024, orc.TWO_PI, P_), (16, orc.TWO_PI, P_), (22, 2.0, N_, S_)], orc.FD2),
     "cmid_spectral": orc.Case([(1024, orc.TWO_PI, P_), (10, orc.TWO_PI, P_), (32, 1.0, D_, S_)], orc.SPECTRAL),
 }
