@@ -261,6 +261,13 @@ FP_API fp_status fp_dist_mean_partial(const fp_plan* plan, void* out_local, cons
                                       void* workspace, size_t workspace_bytes, void* stream, double* dev_sum);
 FP_API fp_status fp_dist_mean_subtract(const fp_plan* plan, void* out_local, const int64_t* out_strides,
                                        const double* dev_total, void* stream);
+/* Phase 1 over a chunk of this rank's axis-1 rows [row0, row0 + nrows) of its block
+ * (0 <= row0, row0 + nrows <= exch_n1 / P): the exchange can be pipelined per chunk of
+ * rows -- chunk c's MID while chunk c+1's all-to-all is in flight.  Row chunk c of every
+ * peer block is a contiguous piece of the exchange buffers (rows are outermost in a block). */
+FP_API fp_status fp_solve_mid_rows(const fp_plan* plan, int64_t row0, int64_t nrows, void* xbuf,
+                                   void* workspace, size_t workspace_bytes, void* stream,
+                                   fp_solve_info* dev_info);
 FP_API fp_status fp_solve_phase(const fp_plan* plan, int phase,
                                 const void* rhs, int rhs_dtype, const int64_t* rhs_strides,
                                 void* out, const int64_t* out_strides, void* xbuf,

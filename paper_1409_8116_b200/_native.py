@@ -132,6 +132,9 @@ SIGNATURES = {
         c_int, [c_void_p, c_void_p, POINTER(c_int64), c_void_p, c_size_t, c_void_p, c_void_p],
     ),
     "fp_dist_mean_subtract": (c_int, [c_void_p, c_void_p, POINTER(c_int64), c_void_p, c_void_p]),
+    "fp_solve_mid_rows": (
+        c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p],
+    ),
     "fp_event_create": (c_int, [POINTER(c_void_p)]),
     "fp_event_create_on": (c_int, [c_int, POINTER(c_void_p)]),
     "fp_event_destroy": (c_int, [c_void_p]),

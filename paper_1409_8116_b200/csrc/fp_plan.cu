@@ -1277,7 +1277,8 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                             void* out, const int64_t* out_strides, void* workspace, size_t workspace_bytes,
                             void* stream, fp_solve_info* dev_info, void* const* phase_events,
                             void* const* pass_events, void* xbuf, int ph_lo, int ph_hi,
-                            const Producer* prod = nullptr, const void* ovr = nullptr) {
+                            const Producer* prod = nullptr, const void* ovr = nullptr, long long mid_row0 = 0,
+                            long long mid_rows = -1) {
     if (!P) return fail(FP_ERR_VALUE, "plan is NULL");
     static const char* const kRange[3][3] = {{"fp_solve_phase 0", "fp_solve_phases 0-1", "fp_solve"},
                                              {"", "fp_solve_phase 1", "fp_solve_phases 1-2"},
@@ -1432,6 +1433,27 @@ static fp_status solve_impl(const fp_plan* P, const void* rhs, int rhs_dtype, co
                 }
                 if (d == 3) { g.a_off = (int)(P->rank * P->B); g.a_lim = (int)P->e1; }
                 else { g.b_off = (int)(P->rank * P->B); g.b_lim = (int)P->e1; }
+                if (mid_rows >= 0) {
+                    // a chunk of this rank's axis-1 rows (pipelined exchange): the a axis in 3D,
+                    // the b axis in 2D; global indices keep the eigenvalues and the null line
+                    const size_t eb = (size_t)(g.in_type == ET_C128 || g.in_type == ET_C64 ? 2 : 1) * (P->f32 ? 4 : 8);
+                    if (d == 3) {
+                        g.in = (const char*)g.in + mid_row0 * g.in_sa * eb;
+                        g.out = (char*)g.out + mid_row0 * g.out_sa * eb;
+                        g.a_off += (int)mid_row0;
+                        p.g.na = (int)mid_rows;
+                    } else {
+                        const long long u = g.pair_b ? 2 : 1;   // real view: b counts real lines
+                        g.in = (const char*)g.in + mid_row0 * g.in_sb * eb;
+                        g.out = (char*)g.out + mid_row0 * g.out_sb * eb;
+                        g.b_off += (int)mid_row0;
+                        p.g.nb = (int)(u * mid_rows);
+                    }
+                    g.na = p.g.na; g.nb = p.g.nb;
+                    p.nbt = (p.g.nb + p.lines - 1) / p.lines;
+                    p.tiles = p.g.na * p.nbt;
+                    if (mid_row0 > 0) p.s.dc_out = nullptr;
+                }
             }
             p.g = g;
             p.nonfinite = first && dev_info ? &dev_info->nonfinite : nullptr;
@@ -1523,6 +1545,14 @@ FP_API fp_status fp_plan_spectrum(const fp_plan* P, int64_t ext[3], int* r_axis)
     for (int a = 0; a < 3; ++a) ext[a] = a < P->ndim ? P->cext[a] : 1;
     *r_axis = P->r_axis;
     return FP_OK;
+}
+
+FP_API fp_status fp_solve_mid_rows(const fp_plan* P, int64_t row0, int64_t nrows, void* xbuf, void* workspace,
+                                   size_t workspace_bytes, void* stream, fp_solve_info* dev_info) {
+    if (!P || P->nranks < 2) return fail(FP_ERR_VALUE, "fp_solve_mid_rows: distributed plans only");
+    if (row0 < 0 || nrows < 1 || row0 + nrows > P->B) return fail(FP_ERR_VALUE, "row range outside this rank's block");
+    return solve_impl(P, nullptr, 0, nullptr, nullptr, nullptr, workspace, workspace_bytes, stream, dev_info, nullptr,
+                      nullptr, xbuf, 1, 1, nullptr, nullptr, row0, nrows);
 }
 
 FP_API fp_status fp_solve_phase(const fp_plan* P, int phase, const void* rhs, int rhs_dtype,

@@ -110,6 +110,13 @@ class NativeBackend:
     def middle(self):
         self._ws1 = self._call(1, None, None, self.recv)
 
+    def middle_rows(self, row0, nrows):
+        """Phase 1 on axis-1 rows [row0, row0 + nrows) of this rank's block (pipelined exchange)."""
+        ws, nws = self._workspace(True)
+        nat.check(self._lib.fp_solve_mid_rows(self._handle, int(row0), int(nrows), self.recv.data_ptr(), ws.data_ptr(),
+                                              nws, dv.stream_handle(self.device), self.status.data_ptr()))
+        self._ws_rows = ws
+
     def backward(self, out_local):
         self._ws2 = self._call(2, None, out_local, self.send)
 
@@ -149,11 +156,16 @@ class DistributedSolverPlan:
     the global ``SolveReport`` (identical on every rank).
     """
 
-    def __init__(self, config: SolverConfig, group=None, device=None, backend=None):
+    def __init__(self, config: SolverConfig, group=None, device=None, backend=None, chunks=None):
+        import os
+
         import torch.distributed as dist
 
         self.config = config
         self.group = group
+        # pipelined exchange: the MID of axis-1 row chunk c runs while chunk c+1 is in flight
+        # (FP_DIST_CHUNKS, default 4; 1 = the two whole all-to-alls)
+        self.chunks = int(chunks if chunks is not None else os.environ.get("FP_DIST_CHUNKS", "4"))
         self.nranks = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self._single = None
@@ -200,11 +212,16 @@ class DistributedSolverPlan:
         mark(0)
         be.forward(rhs_local, out_local)
         mark(1)
-        dist.all_to_all_single(be.recv, be.send, group=self.group)
-        mark(2)
-        be.middle()
-        mark(3)
-        dist.all_to_all_single(be.send, be.recv, group=self.group)
+        B = int(self.info.block_n1)
+        C = max(1, min(self.chunks, B))
+        if C == 1 or events is not None:
+            dist.all_to_all_single(be.recv, be.send, group=self.group)
+            mark(2)
+            be.middle()
+            mark(3)
+            dist.all_to_all_single(be.send, be.recv, group=self.group)
+        else:
+            self._pipelined_exchange(be, B, C)
         mark(4)
         be.backward(out_local)
         mark(5)
@@ -213,6 +230,44 @@ class DistributedSolverPlan:
             dist.all_reduce(total, op=dist.ReduceOp.SUM, group=self.group)
             be.subtract_mean(out_local, total)
         return out_local
+
+    def _pipelined_exchange(self, be, B, C):
+        """Both exchanges and the MID in C chunks of axis-1 rows: chunk c is row range
+        [c B/C, (c+1) B/C) of every peer's block -- one contiguous piece per peer -- so
+        each chunk is a batch of point-to-point sends / receives (NCCL group) issued
+        asynchronously; the MID of chunk c waits only for chunk c's receives, and chunk
+        c's return exchange overlaps the MID of chunk c + 1."""
+        import torch.distributed as dist
+
+        P, r = self.nranks, self.rank
+        blk = be.send.numel() // P                 # bytes per peer block
+        row = blk // B                              # bytes per axis-1 row of a block
+        bounds = [(c * B // C, (c + 1) * B // C) for c in range(C)]
+
+        def exchange(src, dst, c):
+            a, b = bounds[c]
+            ops = []
+            for q in range(P):
+                s_view = src[q * blk + a * row: q * blk + b * row]
+                d_view = dst[q * blk + a * row: q * blk + b * row]
+                if q == r:
+                    d_view.copy_(s_view)   # own block
+                else:
+                    ops.append(dist.P2POp(dist.isend, s_view, q, group=self.group))
+                    ops.append(dist.P2POp(dist.irecv, d_view, q, group=self.group))
+            return dist.batch_isend_irecv(ops) if ops else []
+
+        fwd = [exchange(be.send, be.recv, c) for c in range(C)]
+        back = []
+        for c in range(C):
+            for w in fwd[c]:
+                w.wait()
+            a, b = bounds[c]
+            be.middle_rows(a, b - a)
+            back.append(exchange(be.recv, be.send, c))
+        for ws_ in back:
+            for w in ws_:
+                w.wait()
 
     def solve(self, rhs_local, out_local=None):
         import torch.distributed as dist

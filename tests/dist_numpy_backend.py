@@ -127,6 +127,25 @@ class NumpyBackend:
         for s in range(self.P):
             blocks[s][:, : self.a0s[s]] = np.swapaxes(g[self.offs[s]:self.offs[s] + self.a0s[s]], 0, 1)
 
+    def middle_rows(self, row0, nrows):
+        """Phase 1 on a chunk of axis-1 rows: the whole MID on a private copy of the receive
+        buffer (lines are independent), then only rows [row0, row0 + nrows) of every source
+        block written back -- the other chunks' rows may still be arriving."""
+        live = self.recv
+        self.recv = live.clone()
+        status = self.status.copy()
+        try:
+            self.middle()
+            done = self._view(self.recv)
+        finally:
+            self.recv = live
+        if row0 > 0:   # only the chunk holding row 0 carries the null coefficient
+            self.status[:] = status
+        r = self._view(live)
+        blocks = r.reshape((self.P, self.B) + r.shape[1:])
+        dblocks = done.reshape((self.P, self.B) + done.shape[1:])
+        blocks[:, row0:row0 + nrows] = dblocks[:, row0:row0 + nrows]
+
     def backward(self, out_local):
         s = self._view(self.send)
         x = np.swapaxes(s[: self.e1, : self.a0], 0, 1)

@@ -63,6 +63,45 @@ def emulate(config, P, rhs):
     return torch.cat(outs, dim=0), dc, nonfinite
 
 
+def emulate_chunked(config, P, rhs, C):
+    """The pipelined exchange (DistributedSolverPlan._pipelined_exchange) emulated: per chunk of
+    axis-1 rows, the chunk's pieces of every peer block copied, the MID on those rows
+    (fp_solve_mid_rows), the pieces copied back."""
+    import torch
+    from paper_1409_8116_b200.distributed import NativeBackend
+
+    bes = [NativeBackend(config, P, r) for r in range(P)]
+    outs = []
+    for r, be in enumerate(bes):
+        out = be.new_output()
+        off, a0 = int(be.info.offset0), int(be.info.local_n0)
+        be.forward(rhs[off:off + a0].contiguous(), out)
+        outs.append(out)
+    B = int(bes[0].info.block_n1)
+    C = max(1, min(C, B))   # (as DistributedSolverPlan does: no empty chunks)
+    blk = bes[0].send.numel() // P
+    row = blk // B
+    for c in range(C):
+        a, b = c * B // C, (c + 1) * B // C
+        for r in range(P):
+            for s in range(P):
+                bes[r].recv[s * blk + a * row:s * blk + b * row].copy_(bes[s].send[r * blk + a * row:r * blk + b * row])
+        for be in bes:
+            be.middle_rows(a, b - a)
+        for r in range(P):
+            for s in range(P):
+                bes[s].send[r * blk + a * row:r * blk + b * row].copy_(bes[r].recv[s * blk + a * row:s * blk + b * row])
+    for r, be in enumerate(bes):
+        be.backward(outs[r])
+    if bes[0].exact_mean:
+        total = sum(be.local_sum(outs[r]) for r, be in enumerate(bes))
+        for r, be in enumerate(bes):
+            be.subtract_mean(outs[r], total)
+    torch.cuda.synchronize()
+    dc = sum(float(be.read_status()[0]) for be in bes)
+    return torch.cat(outs, dim=0), dc
+
+
 SMALL = {
     "c3": orc.Case([(64, 1.0, orc.NEUMANN, orc.STAGGERED), (32, 1.0, orc.NEUMANN, orc.STAGGERED), (32, 1.0, orc.NEUMANN, orc.STAGGERED)], orc.FD2),
     "c4": orc.Case([(64, orc.TWO_PI, orc.PERIODIC), (64, orc.TWO_PI, orc.PERIODIC), (32, 2.0, orc.NEUMANN, orc.STAGGERED)], orc.FD2),
@@ -109,6 +148,29 @@ def test_dist_emulated_matches_single_gpu(name, P, torch_cuda, rng):
         np_prod = np.prod([a.n for a in case.axes if a.bc == orc.PERIODIC]) if case.periodic_axes else 1.0
         rm = (dc / np_prod) / plan._null_scale
         assert rm == pytest.approx(rep.removed_mean, abs=1e-6 if case.precision == "single" else 1e-12)
+
+
+@pytest.mark.parametrize("P,C", [(2, 3), (3, 2), (4, 4)])
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_dist_pipelined_exchange_matches_single_gpu(name, P, C, torch_cuda, rng):
+    # the exchange in C chunks of axis-1 rows with the MID per chunk (fp_solve_mid_rows)
+    t = torch_cuda
+    case = SMALL[name]
+    config = _config(case)
+    rhs = rng.standard_normal(case.shape)
+    if case.singular:
+        rhs -= rhs.mean()
+    dt = t.float32 if case.precision == "single" else t.float64
+    rhs_t = t.from_numpy(rhs).to("cuda", dt)
+    want, rep = fp.SolverPlan(config).solve(rhs_t)
+    got, dc = emulate_chunked(config, P, rhs_t, C)
+    tol = 1e-5 if case.precision == "single" else 1e-12
+    err = (t.linalg.vector_norm((got - want).double()) / t.linalg.vector_norm(want.double())).item()
+    assert err <= tol, err
+    if case.singular:
+        plan = fp.SolverPlan(config)
+        np_prod = np.prod([a.n for a in case.axes if a.bc == orc.PERIODIC]) if case.periodic_axes else 1.0
+        assert (dc / np_prod) / plan._null_scale == pytest.approx(rep.removed_mean, abs=1e-6 if case.precision == "single" else 1e-12)
 
 
 @pytest.mark.slow
