@@ -86,5 +86,38 @@ def build(force: bool = False, verbose: bool = False, extra_flags=(), lib_path=N
     return lib_out
 
 
+TORCH_EXT_SRC = CSRC / "fp_torch_ext.cpp"
+TORCH_EXT_PATH = LIB_DIR / "fastpoisson_b200_torch.so"
+
+
+def torch_ext_is_stale() -> bool:
+    return (not TORCH_EXT_PATH.exists()) or TORCH_EXT_SRC.stat().st_mtime > TORCH_EXT_PATH.stat().st_mtime
+
+
+def build_torch_ext(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the PyTorch extension in front of the C ABI (csrc/fp_torch_ext.cpp) into
+    ``lib/fastpoisson_b200_torch.so`` (in-tree: it travels with the kernel library).  It is
+    host C++ only -- it takes tensors, reads the current stream and calls fp_solve through
+    the address Python binds -- so it links libtorch but not the kernel library."""
+    if not force and not torch_ext_is_stale():
+        return TORCH_EXT_PATH
+    from torch.utils import cpp_extension
+
+    bdir = OBJ_DIR / "torch_ext"
+    bdir.mkdir(parents=True, exist_ok=True)
+    LIB_DIR.mkdir(parents=True, exist_ok=True)
+    name = "fastpoisson_b200_torch"
+    cpp_extension.load(name=name, sources=[str(TORCH_EXT_SRC)], build_directory=str(bdir), extra_cflags=["-O2"],
+                       with_cuda=True, is_python_module=False, verbose=verbose)
+    built = bdir / f"{name}.so"
+    if not built.exists():
+        raise RuntimeError(f"torch extension build produced no {built}")
+    tmp = TORCH_EXT_PATH.with_suffix(".so.tmp")
+    shutil.copyfile(built, tmp)
+    os.replace(tmp, TORCH_EXT_PATH)
+    return TORCH_EXT_PATH
+
+
 if __name__ == "__main__":  # pragma: no cover
     print(build(force=True, verbose=True))
+    print(build_torch_ext(force=True, verbose=True))

@@ -1,8 +1,13 @@
-"""ctypes binding of the C ABI in ``include/fastpoisson_b200.h``.
+"""Binding of the C ABI in ``include/fastpoisson_b200.h``.
 
 This is the only place the Python host mirror touches native code.  The
 library is loaded lazily; a missing or unloadable library raises immediately
 (there is no CPU fallback for the solve path).
+
+Two layers: ctypes for plan management and the cold entry points, and the
+PyTorch extension ``lib/fastpoisson_b200_torch.so`` (csrc/fp_torch_ext.cpp) for
+the solve itself -- ``torch.ops.fastpoisson_b200.solve`` takes the tensors,
+reads the current stream and calls ``fp_solve`` of this same library instance.
 """
 
 from __future__ import annotations
@@ -12,7 +17,7 @@ import os
 import threading
 from ctypes import POINTER, Structure, c_double, c_float, c_int, c_int32, c_int64, c_size_t, c_void_p, c_char_p
 
-from ._build import LIB_PATH
+from ._build import LIB_PATH, TORCH_EXT_PATH
 
 FP_OK = 0
 FP_ERR_CONFIG = 1
@@ -167,6 +172,39 @@ def load(path=None):
         if path is None:
             _lib = lib
         return lib
+
+
+_ext_ops = None
+
+
+def torch_ext():
+    """``torch.ops.fastpoisson_b200`` bound to the loaded kernel library (raises if the
+    extension is missing: build it with ``__graft_entry__.build()``).  ``FP_BINDING=ctypes``
+    selects the plain ctypes call instead (A/B and debugging)."""
+    global _ext_ops
+    if _ext_ops is not None:
+        return _ext_ops
+    lib = load()
+    with _lock:
+        if _ext_ops is not None:
+            return _ext_ops
+        import torch
+
+        try:
+            torch.ops.load_library(str(TORCH_EXT_PATH))
+        except (OSError, RuntimeError) as exc:
+            raise RuntimeError(
+                f"PyTorch extension {TORCH_EXT_PATH} is not loadable ({exc}); build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'`"
+            ) from None
+        ops = torch.ops.fastpoisson_b200
+        ops.bind(ctypes.cast(lib.fp_solve, c_void_p).value, ctypes.cast(lib.fp_solve_override, c_void_p).value)
+        _ext_ops = ops
+        return ops
+
+
+def use_torch_ext() -> bool:
+    return os.environ.get("FP_BINDING", "torch") != "ctypes"
 
 
 def last_error() -> str:

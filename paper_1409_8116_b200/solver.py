@@ -357,8 +357,13 @@ class SolverPlan:
             ws = workspace
         else:
             ws = t.empty(max(ws_bytes, 1), dtype=t.uint8, device=self._device)
-        st = stream if stream is not None else dv.stream_handle(self._device)
         ev = events.ev if events is not None else None
+        if stream is None and nat.use_torch_ext():
+            # the PyTorch extension: tensors in, the current stream read natively
+            evp = ctypes.addressof(ev) if ev is not None else 0
+            nat.check(nat.torch_ext().solve(self._handle.value, rhs_t, out_t, ws, info_t, evp, ovr))
+            return ws if ovr is None else (ws, ovr)
+        st = stream if stream is not None else dv.stream_handle(self._device)
         args = (self._handle,
                 rhs_t.data_ptr(), dv.fp_dtype_of_torch(rhs_t.dtype), nat.strides_array(rhs_t.stride()),
                 out_t.data_ptr(), nat.strides_array(out_t.stride()),

@@ -178,3 +178,18 @@ def test_product_never_imports_oracle():
     for p in (ROOT / "paper_1409_8116_b200").rglob("*.py"):
         text = p.read_text()
         assert "import oracle" not in text and "from oracle" not in text, p
+
+
+def test_torch_extension_loads_and_registers_ops(native_lib):
+    # the PyTorch extension in front of the C ABI (csrc/fp_torch_ext.cpp): in-tree, loadable
+    # without a GPU, bound to the loaded kernel library; it has no CPU path
+    import torch
+
+    from paper_1409_8116_b200 import _build
+
+    assert _build.TORCH_EXT_PATH.exists(), "build it: python -c 'import __graft_entry__ as g; g.build()'"
+    ops = _native.torch_ext()
+    assert hasattr(ops, "solve") and hasattr(ops, "bind")
+    z = torch.zeros(4)
+    with pytest.raises(RuntimeError, match="CUDA tensors only"):
+        ops.solve(0, z, z, z, z, 0, None)
