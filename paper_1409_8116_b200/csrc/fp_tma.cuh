@@ -193,8 +193,17 @@ __device__ __forceinline__ void write_makhoul(unsigned char* stg, int lf, int jt
 // smem layout of a TMA tile: [line table][pad to 1024][max(padded tile, staging)][mbarrier]
 template <int LOGM>
 __host__ __device__ constexpr size_t tma_stage_bytes() { return (size_t)(2 << LOGM) * 128; }
+// Register-path kernels at M = 256 interleave the two lines of a warp (lane = 2 jt + line
+// parity): a half-warp's 8-byte staging accesses then cover 8 rows x 2 adjacent columns =
+// sixteen distinct 8-byte slots of the swizzled 128-B row instead of 16 rows of one column
+// (rows t and t + 8 share a chunk: a 2-way conflict on every staged read and write, 27 % of
+// the MID's shared-memory wavefronts, profiles/r02/ncu_full_c3_v6_raw.csv).  The FFT
+// exchanges stay conflict-free with a line stride = 4 (mod 8): a quarter-warp's 16-byte
+// accesses are 4 consecutive jt x 2 lines -> chunks (jt + 4 b) mod 8.
+constexpr int kTmaAltLS = 276;
 __host__ __device__ inline size_t tma_region_bytes(const FftPass& p, size_t stage) {
-    const size_t tile = (size_t)p.lines * p.ls * 16;
+    const int ls = (p.logM == 8 && p.ls < kTmaAltLS) ? kTmaAltLS : p.ls;
+    const size_t tile = (size_t)p.lines * ls * 16;
     return tile > stage ? tile : stage;
 }
 __host__ __device__ inline size_t tma_smem_bytes(const FftPass& p, size_t stage) {
@@ -237,10 +246,12 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
     setup_lines<true, OP>(p, blockIdx.x, linfo);
     __syncthreads();
 
-    const int lf = tid >> LOGTL, jt = tid & (TL - 1);
+    constexpr bool ALT = !SMEM && LOGM == 8;   // two interleaved lines per warp (see kTmaAltLS)
     const int lane = tid & 31;
-    const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
-    const int LS = line_stride<T, LOGM, true>(p);
+    const int lf = ALT ? (((tid >> 5) << 1) | (lane & 1)) : (tid >> LOGTL);
+    const int jt = ALT ? (lane >> 1) : (tid & (TL - 1));
+    const int partner = ALT ? ((((TL - jt) & (TL - 1)) << 1) | (lane & 1)) : ((lane & ~(TL - 1)) | ((TL - jt) & (TL - 1)));
+    const int LS = ALT ? kTmaAltLS : line_stride<T, LOGM, true>(p);
     cx<T>* line_f = sm + lf * LS;
     const void* __restrict__ W = p.wfft;
     const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
