@@ -82,6 +82,30 @@ FftKernelFn tma_kernel(const FftPass& p) {
     return sm ? fft_pass_tma<LOGM, mid_op(FK_DCT2), true> : fft_pass_tma<LOGM, mid_op(FK_DCT2)>;
 }
 
+int sm_count_cached() {
+    static int cnt[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    int& c = cnt[dev & 63];
+    if (c == 0) {
+        int v = 0;
+        c = (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) ? v : 148;
+    }
+    return c;
+}
+
+// L2 prefetch distance (FP_TMA_PF_FWD / _INV / _MID, in tiles per SM; defaults 0 / 2 / 0): a CTA
+// prefetches the input of tile blockIdx.x + distance x #SMs into L2.  At two CTAs per SM a
+// distance of 2 is one resident wave ahead: the tile the CTA that replaces this one will load.
+// Measured on c3 (profiles/r02/ab_l2_prefetch.txt): the inverse pass (two CTAs per SM, exposed
+// load latency) gains 10 %; the forward pass (three CTAs per SM, already at 94 % of the copy
+// bandwidth) and the MID lose at every distance.
+int pf_distance(int op) {
+    // (percent of the SM count)
+    static const int w[3] = {env_mode("FP_TMA_PF_FWD", 100), env_mode("FP_TMA_PF_INV", 100), env_mode("FP_TMA_PF_MID", 0)};   // PassOp order
+    return w[op] > 0 ? (w[op] * sm_count_cached() + 50) / 100 : 0;
+}
+
 FftKernelFn tma_kernel_for(const FftPass& p) {
     switch (p.logM) {
         case 7: return tma_kernel<7>(p);
@@ -199,6 +223,8 @@ bool tma_prepare(FftPass& p, bool f32) {
     if (!encode_real(&p.tm_in, g.in, g.nb, nreal, g.na, g.in_st, g.in_sa, phase_in, &td_in)) return false;
     if (!encode_real(&p.tm_out, g.out, g.nb, nreal, g.na, g.out_st, g.out_sa, phase_out, &td_out)) return false;
     if (td_in != td_out) return false;
+    int td_aux = 0;   // NATURAL view of the input for the L2 prefetch of a later tile
+    if (!encode_real(&p.tm_aux, g.in, g.nb, nreal, g.na, g.in_st, g.in_sa, false, &td_aux) || td_aux != td_in) return false;
     p.tm_tdim = td_in;
     p.tma = 1;
     return true;
@@ -227,7 +253,9 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
         const size_t smem = linfo_bytes(p.lines) + 1024 + (tile > cstg ? tile : cstg) + 16;
         const cudaError_t e = ensure_smem_attr((const void*)fn);
         if (e != cudaSuccess) return e;
-        return launch_pass(fn, dim3(p.tiles), dim3(p.lines << (p.logM - 4)), smem, st, p);
+        FftPass q = p;
+        q.pf_tiles = pf_distance(p.op);
+        return launch_pass(fn, dim3(p.tiles), dim3(p.lines << (p.logM - 4)), smem, st, q);
     }
     FftKernelFn fn = tma_kernel_for(p);
     if (!fn) return cudaErrorInvalidValue;
@@ -235,7 +263,9 @@ cudaError_t launch_fft_tma(const FftPass& p, cudaStream_t st) {
     const cudaError_t e = ensure_smem_attr((const void*)fn);
     if (e != cudaSuccess) return e;
     const int threads = p.lines << (p.logM - 4);
-    return launch_pass(fn, dim3(p.tiles), dim3(threads), smem, st, p);
+    FftPass q = p;
+    q.pf_tiles = pf_distance(p.op);
+    return launch_pass(fn, dim3(p.tiles), dim3(threads), smem, st, q);
 }
 
 }  // namespace fpb

@@ -47,6 +47,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                  ::"r"(smem_addr(dst)), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)) : "memory");
 }
+// L2 prefetch of one box (no shared-memory destination, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
                  ::"l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src)) : "memory");
@@ -104,6 +108,26 @@ __device__ __forceinline__ void tma_issue_load(const FftPass& p, const TmaTile& 
             tma_coords(p, tt, 256 * h, &c1, &c2);
             tma_load_3d(stg + 256 * h * 128, &p.tm_in, tt.c0, c1, c2, bar);
         }
+    }
+}
+// L2 prefetch of the tile `pf_tiles` ahead (the tile a later CTA on this SM will load: its TMA
+// load then hits L2 instead of waiting ~2 us on HBM with the CTA's registers and shared memory idle)
+template <int N>
+__device__ __forceinline__ void tma_issue_prefetch(const FftPass& p) {
+    if (p.pf_tiles <= 0) return;
+    const int t = (int)blockIdx.x + p.pf_tiles;
+    if (t >= p.tiles) return;
+    TmaTile tt;
+    tt.ia = t / p.nbt;
+    tt.c0 = (t % p.nbt) * p.lines;
+    int c1, c2;
+    // always as NATURAL boxes of 256 consecutive rows through tm_aux (element stride 1 over the
+    // input): a prefetch through the PHASE map (traversal stride 4) was measured to cost the
+    // forward pass 20 % -- it appears to fetch the rows between the strided ones as well
+#pragma unroll
+    for (int h = 0; h < N / 256; ++h) {
+        tma_coords(p, tt, 256 * h, &c1, &c2);
+        tma_prefetch_3d(&p.tm_aux, tt.c0, c1, c2);
     }
 }
 template <int N>
@@ -242,6 +266,7 @@ __global__ void __launch_bounds__(256, SMEM ? 3 : 2) fft_pass_tma(const __grid_c
     if (tid == 0) {
         mbar_init(bar, 1);
         tma_issue_load<n>(p, tt, stg, bar, kFwdIn);
+        tma_issue_prefetch<n>(p);
     }
     setup_lines<true, OP>(p, blockIdx.x, linfo);
     __syncthreads();
@@ -544,6 +569,19 @@ __global__ void __launch_bounds__(256, 2) fft_pass_tma_r(const __grid_constant__
                     tma_coords(p, tt, phi + 256 * h, &c1, &c2);
                     tma_load_3d(stg + (phi * (n / 2) + 128 * h) * 64, &p.tm_in, tt.c0, c1, c2, bar);
                 }
+            const int tpf = (int)blockIdx.x + p.pf_tiles;   // L2 prefetch of a later tile's real rows
+            if (p.pf_tiles > 0 && tpf < p.tiles) {
+                TmaTile tp;
+                tp.ia = tpf / p.nbt;
+                tp.c0 = (tpf % p.nbt) * p.lines;
+#pragma unroll
+                for (int phi = 0; phi < 2; ++phi)
+#pragma unroll
+                    for (int h = 0; h < n / 256; ++h) {
+                        tma_coords(p, tp, phi + 256 * h, &c1, &c2);
+                        tma_prefetch_3d(&p.tm_in, tp.c0, c1, c2);
+                    }
+            }
         } else {                // NATURAL complex rows 0..M: boxes of 256 rows + one of 8 (tm_aux)
             mbar_expect_tx(bar, (unsigned)(M + 8) * 128u);
 #pragma unroll
@@ -553,6 +591,20 @@ __global__ void __launch_bounds__(256, 2) fft_pass_tma_r(const __grid_constant__
             }
             tma_coords(p, tt, M, &c1, &c2);
             tma_load_3d(stg + M * 128, &p.tm_aux, 2 * tt.c0, c1, c2, bar);
+            // L2 prefetch of the half spectrum of the tile one resident wave ahead
+            const int tpf = (int)blockIdx.x + p.pf_tiles;
+            if (p.pf_tiles > 0 && tpf < p.tiles) {
+                TmaTile tp;
+                tp.ia = tpf / p.nbt;
+                tp.c0 = (tpf % p.nbt) * p.lines;
+#pragma unroll
+                for (int h = 0; h < M / 256; ++h) {
+                    tma_coords(p, tp, 256 * h, &c1, &c2);
+                    tma_prefetch_3d(&p.tm_in, 2 * tp.c0, c1, c2);
+                }
+                tma_coords(p, tp, M, &c1, &c2);
+                tma_prefetch_3d(&p.tm_aux, 2 * tp.c0, c1, c2);
+            }
         }
     }
     setup_lines<true, OP>(p, blockIdx.x, linfo);

@@ -115,6 +115,7 @@ struct FftPass {
     // TMA-staged strided pass (fp_tma.cu): tensor maps of the in / out arrays, filled at
     // solve time by tma_prepare; tm_tdim = the map dimension of the transform axis
     int tma, tm_tdim;
+    int pf_tiles;               // TMA kernels: L2-prefetch tile blockIdx.x + pf_tiles while this tile computes (0 = off)
     CUtensorMap tm_in, tm_out;
     CUtensorMap tm_aux;         // real-FFT passes: 8-row boxes of the complex half spectrum (row M)
 };
