@@ -115,8 +115,18 @@ __device__ __forceinline__ void setup_lines(const FftPass& p, int tile, LineInfo
     if (!STRIDED) {
         const long long l = (long long)tile * p.lines + tid;
         valid = l < (long long)g.na * g.nb;
-        ia = valid ? (int)(l / g.nb) : 0;
-        ib = valid ? (int)(l % g.nb) : 0;
+        ia = 0;
+        ib = 0;
+        if (valid) {
+            if (l <= 0x7fffffffLL) {   // (a 64-bit divide is ~100 instructions: a third of a one-warp CTA's setup)
+                const unsigned lu = (unsigned)l;
+                ia = (int)(lu / (unsigned)g.nb);
+                ib = (int)(lu - (unsigned)ia * (unsigned)g.nb);
+            } else {
+                ia = (int)(l / g.nb);
+                ib = (int)(l % g.nb);
+            }
+        }
     } else {
         ia = tile / p.nbt;
         ib = (tile % p.nbt) * p.lines + tid;

@@ -186,7 +186,7 @@ static bool tma_prepare_z(FftPass& p) {
     if (!(fwd || inv) || p.logM != 8 || p.lines != 2 || p.family != FAM_CONTIG) return false;
     if (g.blk_lg > 0 || g.row_tab || g.pair_b || g.a_lim > 0 || g.b_lim > 0 || p.prod.active) return false;
     if (g.in_type != ET_F64 || g.out_type != ET_F64 || g.in_st != 1 || g.out_st != 1) return false;
-    if (g.nb % p.lines) return false;
+    if (g.nb % p.lines || (long long)g.na * g.nb > 0x7fffffffLL) return false;
     auto ok16 = [](long long s) { return (s * 8) % 16 == 0; };
     if ((g.nb > 1 && (!ok16(g.in_sb) || !ok16(g.out_sb))) || (g.na > 1 && (!ok16(g.in_sa) || !ok16(g.out_sa)))) return false;
     if (((uintptr_t)g.in % 16) || ((uintptr_t)g.out % 16)) return false;

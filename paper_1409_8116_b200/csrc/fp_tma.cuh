@@ -832,8 +832,9 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
     const size_t tile = (size_t)p.lines * S::LS * 16, sbytes = (size_t)p.lines * n * 8;
     uint64_t* bar = reinterpret_cast<uint64_t*>(stg + (tile > sbytes ? tile : sbytes));
     const int tid = threadIdx.x;
-    const long long l0 = (long long)blockIdx.x * p.lines;
-    const int ia = (int)(l0 / p.g.nb), ib0 = (int)(l0 % p.g.nb);
+    // (tma_prepare_z admits only line counts below 2^31: 32-bit divides)
+    const unsigned l0 = blockIdx.x * (unsigned)p.lines;
+    const int ia = (int)(l0 / (unsigned)p.g.nb), ib0 = (int)(l0 - (unsigned)ia * (unsigned)p.g.nb);
     if (tid == 0) {
         mbar_init(bar, 1);
         mbar_expect_tx(bar, (unsigned)sbytes);
