@@ -24,6 +24,10 @@ CASES = {
     "wall_first_pass": orc.Case([(512, 1.0, N_, S_), (48, orc.TWO_PI, P_), (32, orc.TWO_PI, P_)], orc.SPECTRAL),
     "c3_quarter": orc.Case([(128, 1.0, N_, S_), (256, 1.0, N_, S_), (512, 1.0, N_, S_)], orc.FD2),
     "dst_c3_like": orc.Case([(256, 1.0, D_, S_), (512, 1.0, D_, S_), (64, 1.0, D_, S_)], orc.SPECTRAL),
+    # 512-point DST MID and inverse on the interleaved-lines mapping (two lines per warp), > 148 tiles
+    # along the strided passes so the L2 prefetch of a later tile fires
+    "dst_mid512_3d": orc.Case([(512, 1.0, D_, S_), (56, 1.0, D_, S_), (48, 1.5, D_, S_)], orc.FD2),
+    "neu_y512_many_tiles": orc.Case([(64, 1.0, N_, S_), (512, 1.0, N_, S_), (48, 1.0, N_, S_)], orc.FD2),
     # c4's pattern: the real-FFT axis (1024 points) strided between the wall axis and the MID:
     # the real-FFT forward / inverse on the TMA kernel (8-column tiles, ragged: 36 columns)
     "rfft_c4_like": orc.Case([(16, orc.TWO_PI, P_), (1024, orc.TWO_PI, P_), (36, 2.0, N_, S_)], orc.FD2),
