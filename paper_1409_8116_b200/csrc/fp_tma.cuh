@@ -853,11 +853,13 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
     const T om = (T)p.out_mult;
     cx<T> v[16], pz[8];
     mbar_wait(bar, 0);
-    if (p.nonfinite && L.valid) {
-        bool bad = false;
+    if constexpr (opb(OP) == OP_INV) {
+        if (p.nonfinite && L.valid) {
+            bool bad = false;
 #pragma unroll
-        for (int i = 0; i < n / TL; ++i) bad |= !finite_t(stg_lin<n>(stg, lf, jt + TL * i));
-        if (bad) *p.nonfinite = 1;
+            for (int i = 0; i < n / TL; ++i) bad |= !finite_t(stg_lin<n>(stg, lf, jt + TL * i));
+            if (bad) *p.nonfinite = 1;
+        }
     }
     if constexpr (opb(OP) == OP_FWD) {
         const bool dst = p.fkind == FK_DST2;
@@ -872,6 +874,15 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
                 if (dst) { a = -a; b = -b; }
             }
             v[s] = mkc<T>(a, b);
+        }
+        // the first pass's non-finite check (solver.py:201-202): the line's 16 threads hold every
+        // element of it exactly once in v[]; 0 * x is NaN for x = NaN / +-Inf, so one fused
+        // multiply-add per value and one test replace a second read of the staged line
+        if (p.nonfinite && L.valid) {
+            T acc = (T)0;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) acc = fma(v[s].x, (T)0, fma(v[s].y, (T)0, acc));
+            if (acc != (T)0) *p.nonfinite = 1;
         }
         fft_tile_reg_reg<false, T, LOGM, kTwPow<T, OP>>(line_f, jt, W, v);
         fetch_mirror<T>(v, pz, jt, partner);

@@ -79,6 +79,23 @@ def test_tma_first_pass_nonfinite(torch_cuda, rng):
         fp.SolverPlan(_config(case)).solve(rhs)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("name", ["z512_dst", "z512_neu_2d"])
+def test_tma_contiguous_first_pass_nonfinite(torch_cuda, rng, name, bad):
+    # the contiguous 512-point first pass checks its inputs through 0 * x accumulated over the
+    # registers that hold the line (NaN and both infinities must trip it, finite data must not)
+    case = CASES[name]
+    plan = fp.SolverPlan(_config(case))
+    rhs = rng.standard_normal(case.shape)
+    plan.solve(rhs)                      # finite: no error
+    idx = tuple(int(v) for v in rng.integers(0, np.array(case.shape)))
+    rhs[idx] = bad
+    with pytest.raises(ValueError):
+        plan.solve(rhs)
+    big = rng.standard_normal(case.shape) * 1e300   # huge but finite values stay legal
+    plan.solve(big)
+
+
 def test_tma_ineligible_strides_fall_back(torch_cuda, rng):
     # a ghost-cell sub-block: rows 8-B aligned only -> the regular strided kernel
     t = torch_cuda
