@@ -799,15 +799,18 @@ __global__ void __launch_bounds__(256, 2) fft_pass_tma_c(const __grid_constant__
 
 // ----------------------------------------------------------------------------
 // Contiguous DCT / DST lines (c3's z passes): L = 2 lines of n = 2M = 512 fp64 per CTA.
-// A 4D tensor map views each line as n/16 rows of 128 B; the CTA's box lands as
-// [line][row][16 doubles] with SWIZZLE_128B.  Forward: the Makhoul pairs (x_4m, x_4m+2)
-// / (x_2n-1-4m, x_2n-3-4m) straight into the first FFT stage, the DCT-II quads back as
-// natural rows; inverse: the DCT-III spectrum read in natural order, the de-Makhoul'd
-// output written back.  Element k of line l at l*n*8 + (k/16)*128 + swizzled chunk.
+// A 4D tensor map views each line as n/16 rows of 128 B; the CTA's box lands UNSWIZZLED as
+// [line][row][16 doubles] = the line in natural order, element k of line l at l*n*8 + 8k.
+// The spectrum side (DCT-II outputs, DCT-III inputs: rows q, n-q, M-q, M+q of consecutive
+// threads) is conflict-free 8-byte accesses at base + immediate.  The time-domain side reads
+// 32 contiguous bytes per half-FFT index m -- x_4m .. x_4m+3 as two 16-byte accesses: the even
+// pair is z_m, the odd pair (x_4m+3, x_4m+1) is z_{M-1-m}, which the thread 15 - jt of the
+// same line holds in slot 15 - s -- and exchanges the odd pairs with one warp shuffle each.
+// (A 128-B-swizzled staging needed ~5 integer instructions of address arithmetic per access:
+// 40 % of the kernel's instructions at 70 % issue utilisation.)
 template <int N>
 __device__ __forceinline__ double& stg_lin(unsigned char* stg, int l, int k) {
-    const int r = k >> 4, c = k & 15;
-    return *reinterpret_cast<double*>(stg + l * (N * 8) + r * 128 + ((((c >> 1) ^ r) & 7) << 4) + ((c & 1) << 3));
+    return *reinterpret_cast<double*>(stg + l * (N * 8) + k * 8);
 }
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
     asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
@@ -845,6 +848,8 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
     const int lf = tid >> LOGTL, jt = tid & (TL - 1);
     const int lane = tid & 31;
     const int partner = (lane & ~(TL - 1)) | ((TL - jt) & (TL - 1));
+    static_assert(TL == 16, "two 512-point lines per warp");
+    const int partner2 = (lane & ~(TL - 1)) | (TL - 1 - jt);   // holds z_{M-1-m} in slot 15 - s
     cx<T>* line_f = sm + lf * S::LS;
     const void* __restrict__ W = p.wfft;
     const cx<T>* __restrict__ Wt = reinterpret_cast<const cx<T>*>(p.wt);
@@ -863,17 +868,20 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
     }
     if constexpr (opb(OP) == OP_FWD) {
         const bool dst = p.fkind == FK_DST2;
+        {
+            cx<T> odd[8];
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int m = jt + TL * s;
-            double a, b;
-            if (s < 8) { a = stg_lin<n>(stg, lf, 4 * m); b = stg_lin<n>(stg, lf, 4 * m + 2); }
-            else {
-                a = stg_lin<n>(stg, lf, 2 * n - 1 - 4 * m);
-                b = stg_lin<n>(stg, lf, 2 * n - 3 - 4 * m);
-                if (dst) { a = -a; b = -b; }
+            for (int s = 0; s < 8; ++s) {
+                const double2* c = reinterpret_cast<const double2*>(stg + lf * (n * 8) + 32 * (jt + TL * s));
+                const double2 c0 = c[0], c1 = c[1];
+                v[s] = mkc<T>(c0.x, c1.x);
+                odd[s] = mkc<T>(c1.y, c0.y);
             }
-            v[s] = mkc<T>(a, b);
+#pragma unroll
+            for (int s = 8; s < 16; ++s) {
+                v[s] = shfl_cx<T>(odd[15 - s], partner2);
+                if (dst) v[s] = mkc<T>(-v[s].x, -v[s].y);
+            }
         }
         // the first pass's non-finite check (solver.py:201-202): the line's 16 threads hold every
         // element of it exactly once in v[]; 0 * x is NaN for x = NaN / +-Inf, so one fused
@@ -943,15 +951,11 @@ __global__ void __maxnreg__(128) fft_pass_tma_z(const __grid_constant__ FftPass 
         __syncthreads();
         const double oo = dst ? -om : om;
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int m = jt + TL * s;
-            if (s < 8) {
-                stg_lin<n>(stg, lf, 4 * m) = v[s].x * om;
-                stg_lin<n>(stg, lf, 4 * m + 2) = v[s].y * om;
-            } else {
-                stg_lin<n>(stg, lf, 2 * n - 1 - 4 * m) = v[s].x * oo;
-                stg_lin<n>(stg, lf, 2 * n - 3 - 4 * m) = v[s].y * oo;
-            }
+        for (int s = 0; s < 8; ++s) {
+            const cx<T> po = shfl_cx<T>(v[15 - s], partner2);   // (x_4m+3, x_4m+1) of this thread's m
+            double2* c = reinterpret_cast<double2*>(stg + lf * (n * 8) + 32 * (jt + TL * s));
+            c[0] = make_double2(v[s].x * om, po.y * oo);
+            c[1] = make_double2(v[s].y * om, po.x * oo);
         }
     }
     fence_async_smem();
