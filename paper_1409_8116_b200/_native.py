@@ -203,8 +203,25 @@ def torch_ext():
         return ops
 
 
+_ext_missing_warned = False
+
+
 def use_torch_ext() -> bool:
-    return os.environ.get("FP_BINDING", "torch") != "ctypes"
+    """The solve goes through the PyTorch extension unless ``FP_BINDING=ctypes`` -- or the
+    extension was never built, in which case the same C ABI entry point is called through
+    ctypes (same kernels, same library; a warning says so once)."""
+    global _ext_missing_warned
+    if os.environ.get("FP_BINDING", "torch") == "ctypes":
+        return False
+    if _ext_ops is None and not TORCH_EXT_PATH.exists():
+        if not _ext_missing_warned:
+            import warnings
+
+            warnings.warn(f"{TORCH_EXT_PATH} not built: calling fp_solve through ctypes "
+                          "(build it with `python -c 'import __graft_entry__ as g; g.build()'`)", RuntimeWarning)
+            _ext_missing_warned = True
+        return False
+    return True
 
 
 def last_error() -> str:
