@@ -31,6 +31,10 @@ def native_lib():
     from paper_1409_8116_b200 import _build, _native
 
     _build.build()
+    if not cuda_ok():
+        # (a CPU container has the toolchain: build the PyTorch extension too if it is stale;
+        # the GPU box only ever uses the prebuilt files)
+        _build.build_torch_ext()
     return _native.load()
 
 
