@@ -101,14 +101,24 @@ def build_torch_ext(force: bool = False, verbose: bool = False) -> Path:
     the address Python binds -- so it links libtorch but not the kernel library."""
     if not force and not torch_ext_is_stale():
         return TORCH_EXT_PATH
-    from torch.utils import cpp_extension
+    import sys
 
     bdir = OBJ_DIR / "torch_ext"
     bdir.mkdir(parents=True, exist_ok=True)
     LIB_DIR.mkdir(parents=True, exist_ok=True)
     name = "fastpoisson_b200_torch"
-    cpp_extension.load(name=name, sources=[str(TORCH_EXT_SRC)], build_directory=str(bdir), extra_cflags=["-O2"],
-                       with_cuda=True, is_python_module=False, verbose=verbose)
+    # in a child process: cpp_extension.load also LOADS what it built, and a second copy of the
+    # same TORCH_LIBRARY (lib/..., loaded by _native.torch_ext) in one process aborts
+    code = (
+        "from torch.utils import cpp_extension\n"
+        f"cpp_extension.load(name={name!r}, sources=[{str(TORCH_EXT_SRC)!r}], build_directory={str(bdir)!r}, "
+        f"extra_cflags=['-O2'], with_cuda=True, is_python_module=False, verbose={bool(verbose)!r})\n"
+    )
+    proc = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    if verbose:
+        print(proc.stdout, proc.stderr, flush=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"torch extension build failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
     built = bdir / f"{name}.so"
     if not built.exists():
         raise RuntimeError(f"torch extension build produced no {built}")
